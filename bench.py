@@ -1,0 +1,415 @@
+"""Benchmark: D-iteration PageRank on one B200 per rank (BASELINE.json metric).
+
+metric  edges diffused/s and time to L1 residual 1e-9 (100M nodes), % of HBM peak
+step    one full solve: init F=(1-d)/N, H=0; device sweeps until the fluid mass
+        R satisfies R/(1-d) <= 1e-9; normalize the history into the rank.
+value   elementary steps (edges diffused, PAPER sec. 4.2) of all ranks / max-over-ranks
+        device time, with the graph resident in HBM.
+e2e     the same metric through the C-ABI host-buffer entry fr_pagerank_host:
+        H2D of the CSR from pinned memory, solve, D2H of the rank, per step.
+Multi-GPU: the solve does not shard (one graph per GPU, BASELINE north star),
+so --gpus N runs N independent replicas ("replicas only", scaling = weak).
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port of engine.run + ThresholdSweepScheduler, bit-exact with the
+reference) on a bounded sample of the workload, on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "edges diffused/s and time to L1 residual 1e-9 (100M nodes), % of HBM peak"
+UNIT = "edges/s"
+
+WORKLOADS = {
+    # BASELINE.json configs[4]: N=100M, ~1.6B edges (mean out-degree 16), int64 offsets, uint32 columns
+    5: dict(n=100_000_000, mean=16.0, damping=0.85, target=1e-9,
+            name="config5: web graph N=100M, mean out-degree 16 (power law 2.1, 15% dangling, "
+                 "70% local +-1000 / 30% Zipf(1.0)), d=0.85, fp64, L1 residual 1e-9"),
+    3: dict(n=20_000_000, mean=10.0, damping=0.85, target=1e-9,
+            name="config3: web graph N=20M, mean out-degree 10, d=0.85, fp64, L1 residual 1e-9"),
+    2: dict(n=1_000_000, mean=8.0, damping=0.85, target=1e-9,
+            name="config2: web graph N=1M, mean out-degree 8, d=0.85, fp64, L1 residual 1e-9"),
+}
+CPU_SAMPLE_N = 1_000_000
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def reduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ CPU baseline
+def cpu_sample(seconds_cap=None):
+    """Reference algorithm (oracle port, bit-exact with fluidrank.engine.run + sweep scheduler)
+    on the config-5 generator scaled to N=1M nodes: one full solve to residual 1e-9."""
+    from oracle import oracle as O
+    O.build()
+    w = WORKLOADS[5]
+    src, dst = O.gen_edges(O.web_config(w["mean"]), CPU_SAMPLE_N, 1)
+    off, tgt, stats = O.csr_build(CPU_SAMPLE_N, src, dst, clean=True)
+    del src, dst
+    t0 = time.perf_counter()
+    r = O.run_seq(off, tgt, w["damping"], w["target"], "sweep")
+    dt = time.perf_counter() - t0
+    return {"value": r.elementary_steps / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": (f"config-5 generator scaled to N={CPU_SAMPLE_N:,} (L={stats[0]:,}), one full solve "
+                       f"to residual 1e-9: {r.elementary_steps:,} edges in {dt:.2f} s, sequential "
+                       "ALGO-REF + ThresholdSweepScheduler (oracle/fr_oracle.c, bit-exact with the reference)"),
+            "seconds": dt, "elementary_steps": r.elementary_steps}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_sample()
+    vals, secs, steps = [], [], 0
+    for _ in range(args.steps):
+        s = cpu_sample()
+        vals.append(s["value"])
+        secs.append(s["seconds"])
+        steps += s["elementary_steps"]
+        last = s
+    total = sum(secs)
+    value = steps / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": last["sample"], "parallelism": "1 host core (sequential algorithm)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": last["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def algorithmic_bytes(n, trace_rows, fp32):
+    """Algorithmic bytes per kernel class over a solve.
+
+    select: every sweep reads F (8 B/node, 4 for fp32); each diffused node
+            writes F (8), reads+writes H (16), reads its two row offsets (16)
+            and writes a queue entry (node 4 + push value 8).
+    push:   per diffused edge: column index 4 B + read-modify-write of the
+            target's fluid (16 B, 8 for fp32); per pushed node: offsets 16 +
+            queue entry 12.
+    """
+    fb = 4 if fp32 else 8
+    sweeps = len(trace_rows)
+    diffusions = trace_rows[-1].diffusions if trace_rows else 0
+    edges = trace_rows[-1].elementary_steps if trace_rows else 0
+    sel = sweeps * n * fb + diffusions * (fb + 16 + 16 + 4 + fb)
+    push = edges * (4 + 2 * fb) + diffusions * (16 + 4 + fb)
+    return sel, push
+
+
+def run_ours(args, world, rank, local):
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_1202_6158_b200 as fr
+    from paper_1202_6158_b200 import _lib, gen
+
+    w = dict(WORKLOADS[args.config])
+    if args.n:
+        w["n"] = args.n
+    n = w["n"]
+    dev = torch.device("cuda", local)
+    t0 = time.perf_counter()
+    cfg = gen.web_config(w["mean"])
+    src, dst = gen.generate_edges(cfg, n, args.seed)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    off, tgt, (L, dups, loops) = fr.csr_build(n, src, dst, clean=True)
+    torch.cuda.synchronize()
+    t_csr = time.perf_counter() - t0
+    slots = src.numel()
+    del src, dst
+    torch.cuda.empty_cache()
+    g = fr.SparseGraph(n, off, tgt)
+    fp32 = args.fluid == "fp32"
+    params = fr.DiffusionParams(damping=w["damping"], target_error=w["target"])
+    sched = fr.make_scheduler("sweep", policy=args.policy, sweep_decay=args.decay,
+                              thread_max_degree=args.thread_max, block_min_degree=args.block_min)
+    state = fr.init(g, params, fluid_dtype=torch.float32 if fp32 else torch.float64)
+    solver = fr.Solver(g, state, sched, params, trace_cap=1 << 16)
+    rank_out = torch.empty(n, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        _lib.check(_lib.lib.fr_init_state(n, params.damping, None, _lib.ptr(state.fluid), int(fp32),
+                                          _lib.ptr(state.history), _lib.stream_ptr()))
+        st = solver.run()
+        _lib.check(_lib.lib.fr_normalize(n, _lib.ptr(state.history), _lib.ptr(rank_out), None,
+                                         _lib.stream_ptr()))
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    edges = 0
+    sweeps = []
+    stats = []
+    for _ in range(args.steps):
+        st = step()
+        edges += st.elementary_steps
+        sweeps.append(st.sweeps)
+        stats.append(st)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    barrier(world)
+    ms = ev0.elapsed_time(ev1)
+    ms_max = reduce_max(ms, world)
+    edges_all = reduce_sum(float(edges), world)
+    value = edges_all / (ms_max / 1000.0)
+    ms_per_step = ms_max / args.steps
+    last = stats[-1]
+    rows = solver.trace_rows()
+    # our kernels in the timed region: init(1) + graph (2 + 5 per sweep) + exact residual (2) + normalize (3)
+    launches = sum(1 + 2 + 5 * s + 2 + 3 for s in sweeps)
+
+    # correctness guard for the measured run: stopping rule met, rank normalized
+    assert last.residual <= params.target_error * (1 - params.damping) * 1.0000001, last.residual
+    rsum = float(rank_out.sum())
+    assert abs(rsum - 1.0) < 1e-9, rsum
+
+    # ---- per-kernel roofline: same solve, launched sweep by sweep with events
+    _lib.check(_lib.lib.fr_init_state(n, params.damping, None, _lib.ptr(state.fluid), int(fp32),
+                                      _lib.ptr(state.history), _lib.stream_ptr()))
+    solver.run(profiled=True)
+    kms, kl = solver.kernel_ms, solver.kernel_launches
+    rows_p = solver.trace_rows()
+    sel_b, push_b = algorithmic_bytes(n, rows_p, fp32)
+    push_ms = kms[1] + kms[2] + kms[3]
+    peak, peak_kind = load_peaks()
+    classes = {"select": (kms[0], kl[0], sel_b), "push": (push_ms, kl[1], push_b)}
+    dom = max(classes, key=lambda k: classes[k][0])
+    dms, dl, db = classes[dom]
+    achieved = (db / dl) / ((dms / dl) / 1000.0) / 1e9 if dl else 0.0
+    traffic = None
+    ncu_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(ncu_path):
+        try:
+            traffic = json.load(open(ncu_path)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": {"select": "k_select", "push": "k_push_thread+k_push_warp+k_push_block"}[dom],
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
+                "bytes_per_launch": db / dl if dl else 0,
+                "avg_launch_ms": dms / dl if dl else 0,
+                "share_of_step": round(dms / sum(kms), 4) if sum(kms) else None,
+                "kernel_ms": {"select": kms[0], "push_thread": kms[1], "push_warp": kms[2],
+                              "push_block": kms[3], "finalize": kms[4]},
+                "bytes_per_diffused_edge": round((sel_b + push_b) / max(1, rows_p[-1].elementary_steps), 2)}
+
+    # ---- end to end through the C ABI from pinned host buffers
+    h_off = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+    h_tgt = torch.empty(L, dtype=torch.int32, pin_memory=True)
+    h_off.copy_(off)
+    h_tgt.copy_(tgt)
+    h_rank = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    cfgc = sched.solver_config(params, fp32)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    hs = _lib.SolveStats()
+    # free the resident copy so the host path allocates its own
+    e2e_edges = 0
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        _lib.check(_lib.lib.fr_pagerank_host(n, L, h_off.data_ptr(), h_tgt.data_ptr(), ctypes.byref(cfgc),
+                                             h_rank.data_ptr(), ctypes.byref(hs)))
+        e2e_edges += hs.elementary_steps
+    e2e_s = time.perf_counter() - t0
+    e2e_s = reduce_max(e2e_s, world)
+    e2e_edges = reduce_sum(float(e2e_edges), world)
+    rank_err = float((h_rank.to(dev) - rank_out).abs().sum())
+
+    line = None
+    if rank == 0:
+        cpu = cpu_sample() if not args.no_cpu else None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32-fluid/f64-history" if fp32 else "f64", "data": "synthetic",
+            "config": {"workload": w["name"], "n": n, "edges": L, "edge_slots_drawn": slots,
+                       "duplicates_dropped": dups, "self_loops_dropped": loops, "damping": w["damping"],
+                       "target_error": w["target"], "policy": args.policy, "decay": args.decay,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (CSR %.1f GB >> 126 MB)" % ((8 * (n + 1) + 4 * L) / 1e9)},
+            "time_to_residual_s": ms_per_step / 1000.0,
+            "sweeps_per_solve": last.sweeps, "diffusions_per_solve": last.diffusions,
+            "edges_per_solve": last.elementary_steps, "final_residual": last.residual,
+            "graph_gen_s": t_gen, "csr_build_s": t_csr,
+            "e2e": {"value": e2e_edges / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * (n + 1) + 4 * L, "d2h_bytes_per_step": 8 * n,
+                    "seconds_per_step": e2e_s / e2e_steps, "steps": e2e_steps,
+                    "rank_l1_vs_resident_run": rank_err},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    barrier(world)
+    solver.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=5, choices=sorted(WORKLOADS))
+    ap.add_argument("--n", type=int, default=0, help="override node count (scaled workload)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--policy", default="exhaust", choices=("exhaust", "geometric", "mass"))
+    ap.add_argument("--decay", type=float, default=0.5)
+    ap.add_argument("--fluid", default="fp64", choices=("fp64", "fp32"))
+    ap.add_argument("--thread-max", type=int, default=0)
+    ap.add_argument("--block-min", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        rc = run_reference(args, world, rank)
+    else:
+        rc = run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,110 @@
+// fr_capi.cu -- error state, device facts and the host-buffer end-to-end entry.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <mutex>
+
+#include "fr_common.cuh"
+
+namespace fr {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
+    set_error("CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e), file, line, what);
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return FR_ERR_NO_DEVICE;
+    return FR_ERR_CUDA;
+}
+
+int device_info(DeviceInfo *out) {
+    static thread_local DeviceInfo cache;
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice", __FILE__, __LINE__);
+    if (cache.device != dev) {
+        DeviceInfo d;
+        d.device = dev;
+        e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute", __FILE__, __LINE__);
+        cudaDeviceGetAttribute(&d.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cache = d;
+    }
+    *out = cache;
+    return FR_OK;
+}
+
+}  // namespace fr
+
+using namespace fr;
+
+extern "C" const char *fr_last_error(void) { return g_err; }
+extern "C" int fr_abi_version(void) { return FR_ABI_VERSION; }
+
+extern "C" int fr_device_sms(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1) {
+        cudaGetLastError();
+        return 0;
+    }
+    DeviceInfo di;
+    return device_info(&di) == FR_OK ? di.sms : 0;
+}
+
+extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, const uint32_t *h_targets,
+                                const fr_solver_config *cfg, double *h_rank, fr_solve_stats *h_stats) {
+    if (n < 1 || m < 0 || !h_offsets || (m > 0 && !h_targets) || !cfg || !h_rank) {
+        set_error("fr_pagerank_host: bad arguments");
+        return FR_ERR_ARG;
+    }
+    cudaStream_t st;
+    FR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int rc = FR_OK;
+    fr_solver *s = nullptr;
+    int64_t *d_off = nullptr;
+    uint32_t *d_tgt = nullptr;
+    double *d_h = nullptr;
+    void *d_f = nullptr;
+    const size_t fsz = cfg->fluid_fp32 ? sizeof(float) : sizeof(double);
+    do {
+        cudaError_t e;
+        if ((e = cudaMallocAsync(&d_off, sizeof(int64_t) * (size_t)(n + 1), st)) != cudaSuccess ||
+            (e = cudaMallocAsync(&d_tgt, sizeof(uint32_t) * (size_t)(m > 0 ? m : 1), st)) != cudaSuccess ||
+            (e = cudaMallocAsync(&d_h, sizeof(double) * (size_t)n, st)) != cudaSuccess ||
+            (e = cudaMallocAsync(&d_f, fsz * (size_t)n, st)) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaMallocAsync", __FILE__, __LINE__);
+            break;
+        }
+        if ((e = cudaMemcpyAsync(d_off, h_offsets, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice, st)) !=
+                cudaSuccess ||
+            (m > 0 && (e = cudaMemcpyAsync(d_tgt, h_targets, sizeof(uint32_t) * (size_t)m, cudaMemcpyHostToDevice,
+                                           st)) != cudaSuccess)) {
+            rc = cuda_fail(e, "cudaMemcpyAsync(H2D)", __FILE__, __LINE__);
+            break;
+        }
+        if ((rc = fr_init_state(n, cfg->damping, nullptr, d_f, cfg->fluid_fp32, d_h, st)) != FR_OK) break;
+        if ((rc = fr_solver_create(n, m, d_off, d_tgt, nullptr, d_f, d_h, cfg, 0, st, &s)) != FR_OK) break;
+        if ((rc = fr_solver_run(s, st, h_stats)) != FR_OK) break;
+        // rank = history / |history|_1, computed in place, then one D2H copy
+        if ((rc = fr_normalize(n, d_h, d_h, nullptr, st)) != FR_OK) break;
+        if ((e = cudaMemcpyAsync(h_rank, d_h, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, st)) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaMemcpyAsync(D2H)", __FILE__, __LINE__);
+            break;
+        }
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) rc = cuda_fail(e, "sync", __FILE__, __LINE__);
+    } while (0);
+    if (s) fr_solver_destroy(s);
+    cudaFreeAsync(d_off, st);
+    cudaFreeAsync(d_tgt, st);
+    cudaFreeAsync(d_h, st);
+    cudaFreeAsync(d_f, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    return rc;
+}

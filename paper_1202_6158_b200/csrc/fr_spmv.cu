@@ -1,0 +1,379 @@
+// fr_spmv.cu -- power iteration (MAT-ITER), the in-repo comparison solver.
+//
+// baseline.py:181-217: x <- v; repeat y = d*P*x + (1-d)*v; y += (1 - sum y)*v;
+// diff = |y - x|_1; x = y; until diff*d/(1-d) <= target.  P*x is a pull SpMV
+// over the transposed CSR (rows = targets, columns = sources ascending, the
+// reference's graph.to_matrix(), graph.py:158-165):
+//   s_i = sum_{j in in(i)} z_j,   z_j = x_j / outdeg_j (0 for dangling j)
+// Short rows: one 8-lane group per row.  Rows longer than LONG_ROW are split
+// into warp-sized segments whose partial sums are combined with atomics.
+// The iteration loop is a CUDA-graph while-node (no host round trip).
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "fr_common.cuh"
+
+namespace fr {
+
+static constexpr int PI_NT = 256;
+static constexpr u64 LONG_ROW = 1024;
+static constexpr u64 SEG = 2048;
+
+struct PiCtl {
+    double c;       // teleport re-injection 1 - sum(y)
+    double diff;
+    double sum_v;
+    u64 iters;
+    u32 stop;
+};
+
+struct PiArgs {
+    long long n;
+    const u64 *in_off;
+    const u32 *in_src;
+    const double *inv;  // 1/outdeg or 0
+    const double *v;
+    double *x, *z, *s;
+    const u64 *seg_row, *seg_lo, *seg_hi;
+    long long nseg;
+    double *part_s, *part_d;
+    int nparts;
+    PiCtl *ctl;
+    double d, target;
+    long long max_iter;
+    int in_graph;
+    cudaGraphConditionalHandle cond;
+};
+
+__global__ void __launch_bounds__(PI_NT) k_pi_init(PiArgs a) {
+    for (long long i = blockIdx.x * (long long)PI_NT + threadIdx.x; i < a.n; i += (long long)gridDim.x * PI_NT) {
+        const double xi = a.v[i];
+        a.x[i] = xi;
+        a.z[i] = xi * a.inv[i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ctl->iters = 0;
+        a.ctl->stop = 0;
+        if (a.in_graph) cudaGraphSetConditional(a.cond, 1u);
+    }
+}
+
+// 8 lanes per row; long rows only get their accumulator cleared here.
+__global__ void __launch_bounds__(PI_NT) k_pi_rows(PiArgs a) {
+    __shared__ double sm[PI_NT / 32];
+    const int sub = threadIdx.x & 7;
+    const long long groups = (long long)gridDim.x * (PI_NT / 8);
+    double acc_block = 0.0;
+    const long long g0 = blockIdx.x * (long long)(PI_NT / 8) + (threadIdx.x >> 3);
+    // uniform trip count so the 8-lane shuffles stay converged
+    const long long trips = (a.n + groups - 1) / groups;
+    for (long long t = 0; t < trips; t++) {
+        const long long i = g0 + t * groups;
+        double acc = 0.0;
+        bool long_row = false;
+        if (i < a.n) {
+            const u64 lo = a.in_off[i], hi = a.in_off[i + 1];
+            long_row = hi - lo > LONG_ROW;
+            if (!long_row)
+                for (u64 k = lo + sub; k < hi; k += 8) acc += a.z[__ldg(a.in_src + k)];
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        if (i < a.n && sub == 0) {
+            a.s[i] = acc;  // 0 for long rows: their segments accumulate next
+            acc_block += acc;
+        }
+    }
+    acc_block = block_sum<PI_NT>(acc_block, sm);
+    if (threadIdx.x == 0) a.part_s[blockIdx.x] = acc_block;
+}
+
+// Warp per segment of a long row.
+__global__ void __launch_bounds__(PI_NT) k_pi_segs(PiArgs a) {
+    __shared__ double sm[PI_NT / 32];
+    const int lane = threadIdx.x & 31;
+    double acc_block = 0.0;
+    const long long nw = (long long)gridDim.x * (PI_NT / 32);
+    for (long long q = blockIdx.x * (long long)(PI_NT / 32) + (threadIdx.x >> 5); q < a.nseg; q += nw) {
+        const u64 lo = a.seg_lo[q], hi = a.seg_hi[q];
+        double acc = 0.0;
+        for (u64 k = lo + lane; k < hi; k += 32) acc += a.z[__ldg(a.in_src + k)];
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            atomicAdd(a.s + a.seg_row[q], acc);
+            acc_block += acc;
+        }
+    }
+    acc_block = block_sum<PI_NT>(acc_block, sm);
+    if (threadIdx.x == 0) a.part_s[a.nparts + blockIdx.x] = acc_block;
+}
+
+__global__ void __launch_bounds__(PI_NT) k_pi_mass(PiArgs a) {
+    __shared__ double sm[PI_NT / 32];
+    double t = 0.0;
+    for (int p = threadIdx.x; p < 2 * a.nparts; p += PI_NT) t += a.part_s[p];
+    t = block_sum<PI_NT>(t, sm);
+    if (threadIdx.x == 0) {
+        const double ysum = a.d * t + (1.0 - a.d) * a.ctl->sum_v;
+        a.ctl->c = 1.0 - ysum;  // baseline.py:206 dangling mass back through v
+    }
+}
+
+__global__ void __launch_bounds__(PI_NT) k_pi_update(PiArgs a) {
+    __shared__ double sm[PI_NT / 32];
+    const double c = a.ctl->c;
+    double diff = 0.0;
+    for (long long i = blockIdx.x * (long long)PI_NT + threadIdx.x; i < a.n; i += (long long)gridDim.x * PI_NT) {
+        const double vi = a.v[i];
+        double y = a.d * a.s[i] + (1.0 - a.d) * vi;
+        y += c * vi;
+        diff += fabs(y - a.x[i]);
+        a.x[i] = y;
+        a.z[i] = y * a.inv[i];
+    }
+    diff = block_sum<PI_NT>(diff, sm);
+    if (threadIdx.x == 0) a.part_d[blockIdx.x] = diff;
+}
+
+__global__ void __launch_bounds__(PI_NT) k_pi_check(PiArgs a) {
+    __shared__ double sm[PI_NT / 32];
+    double t = 0.0;
+    for (int p = threadIdx.x; p < a.nparts; p += PI_NT) t += a.part_d[p];
+    t = block_sum<PI_NT>(t, sm);
+    if (threadIdx.x == 0) {
+        PiCtl *c = a.ctl;
+        c->diff = t;
+        c->iters += 1;
+        const bool done = t * (a.d / (1.0 - a.d)) <= a.target || (long long)c->iters >= a.max_iter;
+        c->stop = done ? 1u : 0u;
+        if (a.in_graph) cudaGraphSetConditional(a.cond, done ? 0u : 1u);
+    }
+}
+
+__global__ void k_pi_inv(long long n, const u64 *__restrict__ off, double *__restrict__ inv) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const u64 d = off[i + 1] - off[i];
+        inv[i] = d ? 1.0 / (double)d : 0.0;
+    }
+}
+__global__ void k_fill(long long n, double v, double *x) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+__global__ void k_long_rows(long long n, const u64 *__restrict__ off, u32 *list, u32 *count) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        if (off[i + 1] - off[i] > LONG_ROW) list[atomicAdd(count, 1u)] = (u32)i;
+}
+
+__global__ void k_row_bounds(const u32 *__restrict__ rows, u32 cnt, const u64 *__restrict__ off, u64 *out) {
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < cnt) {
+        out[2 * k] = off[rows[k]];
+        out[2 * k + 1] = off[rows[k] + 1];
+    }
+}
+
+}  // namespace fr
+
+using namespace fr;
+
+struct fr_power {
+    long long n, m;
+    PiArgs a;
+    double *buf;
+    u64 *segbuf;
+    PiCtl *ctl;
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    double target;
+    long long max_iter;
+    int grid;
+    int seg_grid;
+};
+
+static int add_node(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *dep, void *func, int grid, void **args) {
+    cudaKernelNodeParams p = {};
+    p.func = func;
+    p.gridDim = dim3((unsigned)grid);
+    p.blockDim = dim3(PI_NT);
+    p.kernelParams = args;
+    FR_CUDA(cudaGraphAddKernelNode(node, g, dep, dep ? 1 : 0, &p));
+    return FR_OK;
+}
+
+static int power_build_graph(fr_power *p) {
+    if (p->exec) { cudaGraphExecDestroy(p->exec); p->exec = nullptr; }
+    if (p->graph) { cudaGraphDestroy(p->graph); p->graph = nullptr; }
+    FR_CUDA(cudaGraphCreate(&p->graph, 0));
+    FR_CUDA(cudaGraphConditionalHandleCreate(&p->a.cond, p->graph, 0, 0));
+    p->a.in_graph = 1;
+    p->a.target = p->target;
+    p->a.max_iter = p->max_iter;
+    void *args[] = {&p->a};
+    cudaGraphNode_t n_init, n_while;
+    FR_TRY(add_node(p->graph, &n_init, nullptr, (void *)k_pi_init, p->grid, args));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = p->a.cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    FR_CUDA(cudaGraphAddNode(&n_while, p->graph, &n_init, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaGraphNode_t n1, n2, n3, n4, n5;
+    FR_TRY(add_node(body, &n1, nullptr, (void *)k_pi_rows, p->grid, args));
+    FR_TRY(add_node(body, &n2, &n1, (void *)k_pi_segs, p->grid, args));
+    FR_TRY(add_node(body, &n3, &n2, (void *)k_pi_mass, 1, args));
+    FR_TRY(add_node(body, &n4, &n3, (void *)k_pi_update, p->grid, args));
+    FR_TRY(add_node(body, &n5, &n4, (void *)k_pi_check, 1, args));
+    FR_CUDA(cudaGraphInstantiate(&p->exec, p->graph, 0));
+    return FR_OK;
+}
+
+extern "C" int fr_power_destroy(fr_power *p) {
+    if (!p) return FR_OK;
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    cudaFree(p->buf);
+    cudaFree(p->segbuf);
+    cudaFree(p->ctl);
+    delete p;
+    return FR_OK;
+}
+
+extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offsets, const int64_t *d_in_offsets,
+                               const uint32_t *d_in_sources, double damping, const double *d_teleport, void *stream,
+                               fr_power **out) {
+    if (!out || n < 1 || m < 0 || !d_out_offsets || !d_in_offsets || (m > 0 && !d_in_sources) ||
+        !(damping > 0.0 && damping < 1.0)) {
+        set_error("power iteration requires damping < 1 and a valid graph");
+        return FR_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    DeviceInfo di;
+    FR_TRY(device_info(&di));
+    fr_power *p = new fr_power();
+    p->n = n;
+    p->m = m;
+    int rc = FR_OK;
+    do {
+        PiArgs &a = p->a;
+        a.n = n;
+        a.in_off = reinterpret_cast<const u64 *>(d_in_offsets);
+        a.in_src = d_in_sources;
+        a.d = damping;
+        p->grid = di.sms * 8;
+        a.nparts = p->grid;
+        cudaError_t e;
+        // inv, v, x, z, s + partials
+        if ((e = cudaMalloc(&p->buf, sizeof(double) * (5 * (size_t)n + 3 * (size_t)p->grid))) != cudaSuccess ||
+            (e = cudaMalloc(&p->ctl, sizeof(PiCtl))) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaMalloc(power)", __FILE__, __LINE__);
+            break;
+        }
+        double *inv = p->buf, *v = inv + n;
+        a.inv = inv;
+        a.v = v;
+        a.x = v + n;
+        a.z = a.x + n;
+        a.s = a.z + n;
+        a.part_s = a.s + n;           // 2 * grid (rows + segments)
+        a.part_d = a.part_s + 2 * p->grid;
+        a.ctl = p->ctl;
+        k_pi_inv<<<p->grid, PI_NT, 0, st>>>(n, reinterpret_cast<const u64 *>(d_out_offsets), inv);
+        if (d_teleport) {
+            if ((e = cudaMemcpyAsync(v, d_teleport, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st)) !=
+                cudaSuccess) {
+                rc = cuda_fail(e, "copy teleport", __FILE__, __LINE__);
+                break;
+            }
+        } else {
+            k_fill<<<p->grid, PI_NT, 0, st>>>(n, 1.0 / (double)n, v);
+        }
+        double sum_v = 0.0;
+        if ((rc = fr_abs_sum(n, v, 0, &sum_v, st)) != FR_OK) break;
+        PiCtl hc = {};
+        hc.sum_v = sum_v;
+        if ((e = cudaMemcpyAsync(p->ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+            rc = cuda_fail(e, "ctl", __FILE__, __LINE__);
+            break;
+        }
+        // long-row segments
+        Scratch scratch(st);
+        u32 *d_list, *d_cnt;
+        if ((rc = scratch.alloc(&d_list, (size_t)std::min<long long>(n, m / (long long)LONG_ROW + 1))) != FR_OK) break;
+        if ((rc = scratch.alloc(&d_cnt, 1)) != FR_OK) break;
+        cudaMemsetAsync(d_cnt, 0, sizeof(u32), st);
+        k_long_rows<<<p->grid, PI_NT, 0, st>>>(n, a.in_off, d_list, d_cnt);
+        u32 nlong = 0;
+        cudaMemcpyAsync(&nlong, d_cnt, sizeof(u32), cudaMemcpyDeviceToHost, st);
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "long rows", __FILE__, __LINE__); break; }
+        std::vector<u32> rows(nlong);
+        std::vector<u64> lo(nlong), hi(nlong);
+        std::vector<u64> seg_row, seg_lo, seg_hi;
+        if (nlong) {
+            u64 *d_bounds;
+            if ((rc = scratch.alloc(&d_bounds, 2 * (size_t)nlong)) != FR_OK) break;
+            k_row_bounds<<<(nlong + 255) / 256, 256, 0, st>>>(d_list, nlong, a.in_off, d_bounds);
+            std::vector<u64> bounds(2 * (size_t)nlong);
+            cudaMemcpyAsync(rows.data(), d_list, sizeof(u32) * nlong, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(bounds.data(), d_bounds, sizeof(u64) * 2 * nlong, cudaMemcpyDeviceToHost, st);
+            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "row bounds", __FILE__, __LINE__); break; }
+            for (u32 k = 0; k < nlong; k++) {
+                lo[k] = bounds[2 * k];
+                hi[k] = bounds[2 * k + 1];
+                for (u64 b = lo[k]; b < hi[k]; b += SEG) {
+                    seg_row.push_back(rows[k]);
+                    seg_lo.push_back(b);
+                    seg_hi.push_back(std::min(hi[k], b + SEG));
+                }
+            }
+        }
+        a.nseg = (long long)seg_row.size();
+        if ((e = cudaMalloc(&p->segbuf, sizeof(u64) * (3 * seg_row.size() + 3))) != cudaSuccess) {
+            rc = cuda_fail(e, "segments", __FILE__, __LINE__);
+            break;
+        }
+        a.seg_row = p->segbuf;
+        a.seg_lo = p->segbuf + seg_row.size() + 1;
+        a.seg_hi = p->segbuf + 2 * seg_row.size() + 2;
+        if (a.nseg) {
+            cudaMemcpy((void *)a.seg_row, seg_row.data(), sizeof(u64) * seg_row.size(), cudaMemcpyHostToDevice);
+            cudaMemcpy((void *)a.seg_lo, seg_lo.data(), sizeof(u64) * seg_row.size(), cudaMemcpyHostToDevice);
+            cudaMemcpy((void *)a.seg_hi, seg_hi.data(), sizeof(u64) * seg_row.size(), cudaMemcpyHostToDevice);
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) { rc = cuda_fail(e, "power setup", __FILE__, __LINE__); break; }
+    } while (0);
+    if (rc != FR_OK) {
+        fr_power_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return FR_OK;
+}
+
+extern "C" int fr_power_run(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
+                            int64_t *h_iterations, double *h_diff, void *stream) {
+    if (!p || !(target_error > 0.0) || !d_x) { set_error("fr_power_run: bad arguments"); return FR_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long mi = max_iterations > 0 ? max_iterations : 1000000;
+    if (!p->exec || p->target != target_error || p->max_iter != mi) {
+        p->target = target_error;
+        p->max_iter = mi;
+        FR_TRY(power_build_graph(p));
+    }
+    FR_CUDA(cudaGraphLaunch(p->exec, st));
+    PiCtl hc;
+    FR_CUDA(cudaMemcpyAsync(&hc, p->ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    FR_CUDA(cudaMemcpyAsync(d_x, p->a.x, sizeof(double) * (size_t)p->n, cudaMemcpyDeviceToDevice, st));
+    FR_CUDA(cudaStreamSynchronize(st));
+    if (h_iterations) *h_iterations = (int64_t)hc.iters;
+    if (h_diff) *h_diff = hc.diff;
+    if (hc.diff * (p->a.d / (1.0 - p->a.d)) > target_error) {
+        set_error("no convergence within %lld iterations", mi);
+        return FR_ERR_NO_CONVERGENCE;
+    }
+    return FR_OK;
+}
