@@ -135,6 +135,13 @@ typedef struct fr_solver_config {
     int32_t thread_max_degree;/* bins: deg <= this -> thread per node (0 = default 8)   */
     int32_t block_min_degree; /* deg >= this -> block per node (0 = default 2048)       */
     uint32_t seed;            /* FR_SELECT_RAND                          */
+    int32_t kernel_path;      /* 0: fused warp-tile sweep (select, take and push in one
+                                    kernel; hubs block-per-node) -- default
+                                 1: binned queues (select kernel, then thread / warp /
+                                    block-per-node push kernels)                    */
+    int32_t hot_slots;        /* fused path: pushes into the hot_slots highest in-degree
+                                 nodes are summed per block in shared memory first
+                                 (0 = default 2048, max 2048; -1 = off)             */
 } fr_solver_config;
 
 typedef struct fr_trace_row {

@@ -41,7 +41,8 @@ class SolverConfig(ctypes.Structure):
                 ("max_diffusions", ctypes.c_int64),
                 ("select", ctypes.c_int32), ("policy", ctypes.c_int32),
                 ("fluid_fp32", ctypes.c_int32), ("thread_max_degree", ctypes.c_int32),
-                ("block_min_degree", ctypes.c_int32), ("seed", ctypes.c_uint32)]
+                ("block_min_degree", ctypes.c_int32), ("seed", ctypes.c_uint32),
+                ("kernel_path", ctypes.c_int32), ("hot_slots", ctypes.c_int32)]
 
 
 class TraceRow(ctypes.Structure):

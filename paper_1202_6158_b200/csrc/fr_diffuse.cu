@@ -37,7 +37,7 @@ static constexpr long long SEL_TILE = SEL_NT * SEL_IT;
 static constexpr int FIN_NT = 256;
 static constexpr int BLK_NT = 512;
 static constexpr int BLK_CHUNK = 2048;  // uint32 column indices per stage (8 KB)
-static constexpr int BLK_STAGES = 4;
+static constexpr int BLK_STAGES = 3;
 
 struct SolveCtl {
     double theta;       // threshold of the next sweep
@@ -48,7 +48,11 @@ struct SolveCtl {
     u64 trace_len;
     u32 qcount[3];
     u32 stop;
+    u32 need_check;     // fused path: incremental residual crossed the target, verify exactly
+    u32 pad;
 };
+
+enum { PATH_FUSED = 0, PATH_BINNED = 1 };
 
 template <typename FT>
 struct SweepArgs {
@@ -62,6 +66,8 @@ struct SweepArgs {
     FT *qval[3];
     double *part_mass, *part_abs, *part_max;
     u64 *part_steps, *part_sel;
+    const u32 *slot_node;  // hot slot -> node (fused path)
+    u32 nhot;
     fr_trace_row *trace;
     long long n;
     long long trace_cap;
@@ -71,6 +77,7 @@ struct SweepArgs {
     u32 t0, t2;  // deg <= t0 -> thread bin; deg >= t2 -> block bin
     int select, policy;
     u32 seed;
+    int path;
     int in_graph;
     cudaGraphConditionalHandle cond;
 };
@@ -83,9 +90,11 @@ __device__ __forceinline__ u64 hmix(u64 z) {
 }
 
 // ------------------------------------------------------------------ prologue
+// Exact sum |F| and max score.  guarded: only when the fused path asked for a check.
 template <typename FT>
-__global__ void __launch_bounds__(SEL_NT) k_mass_partials(SweepArgs<FT> a) {
+__global__ void __launch_bounds__(SEL_NT) k_mass_partials(SweepArgs<FT> a, int guarded) {
     __shared__ double sm[SEL_NT / 32];
+    if (guarded && !a.ctl->need_check) return;
     double mass = 0.0, mx = 0.0;
     for (long long i = blockIdx.x * (long long)SEL_NT + threadIdx.x; i < a.n; i += (long long)gridDim.x * SEL_NT) {
         const double af = fabs((double)a.F[i]);
@@ -119,6 +128,221 @@ __global__ void __launch_bounds__(FIN_NT) k_prologue(SweepArgs<FT> a, int nparts
         c->qcount[0] = c->qcount[1] = c->qcount[2] = 0;
         c->stop = (mass <= a.thr || mass == 0.0) ? 1u : 0u;
         if (a.in_graph) cudaGraphSetConditional(a.cond, c->stop ? 0u : 1u);
+    }
+}
+
+// Fused path: exact check of the stopping rule once the incremental residual
+// says we are done (engine.py:290-293 re-derives the residual the same way).
+template <typename FT>
+__global__ void __launch_bounds__(FIN_NT) k_mass_check(SweepArgs<FT> a, int nparts) {
+    __shared__ double sm[FIN_NT / 32];
+    SolveCtl *c = a.ctl;
+    if (!c->need_check) return;
+    double mass = 0.0;
+    for (int p = threadIdx.x; p < nparts; p += FIN_NT) mass += a.part_mass[p];
+    mass = block_sum<FIN_NT>(mass, sm);
+    if (threadIdx.x == 0) {
+        c->residual = mass;
+        c->need_check = 0;
+        const bool done = mass <= a.thr || mass == 0.0 || c->stop;
+        c->stop = done ? 1u : 0u;
+        if (a.in_graph) cudaGraphSetConditional(a.cond, done ? 0u : 1u);
+    }
+}
+
+// ------------------------------------------------------------------ hot targets
+// Zipf in-degree hubs receive a large share of all pushes; red.global.add on
+// one address serialises in its L2 slice (~0.7 G ops/s measured, tools/
+// red_probe.cu), so pushes into the HOT_SLOTS highest in-degree nodes are
+// summed per block in shared memory and flushed once per block.  The solver
+// keeps a private copy of the column indices in which such targets carry
+// HOT_FLAG | slot (slot_node[slot] = node id).
+static constexpr int HOT_SLOTS = 2048;
+static constexpr u32 HOT_FLAG = 0x80000000u;
+
+template <typename FT>
+__device__ __forceinline__ void push_one(FT *__restrict__ F, FT *hot_acc, u32 t, FT v) {
+    if (t & HOT_FLAG) atomicAdd(hot_acc + (t & ~HOT_FLAG), v);  // shared memory
+    else red_add(F + t, v);
+}
+
+template <typename FT>
+__device__ __forceinline__ void hot_clear(FT *hot_acc, u32 nhot, int nt) {
+    for (u32 s = threadIdx.x; s < nhot; s += nt) hot_acc[s] = (FT)0;
+}
+
+template <typename FT>
+__device__ __forceinline__ void hot_flush(FT *__restrict__ F, const FT *hot_acc, const u32 *__restrict__ slot_node,
+                                          u32 nhot, int nt) {
+    for (u32 s = threadIdx.x; s < nhot; s += nt) {
+        const FT x = hot_acc[s];
+        if (x != (FT)0) red_add(F + slot_node[s], x);
+    }
+}
+
+// ------------------------------------------------------------------ fused sweep (default path)
+static constexpr int SW_NT = 256;
+static constexpr int SW_UNROLL = 4;
+
+__device__ __forceinline__ double take_fluid(double *p) {
+    return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
+}
+__device__ __forceinline__ float take_fluid(float *p) { return atomicExch(p, 0.0f); }
+
+__device__ __forceinline__ u32 warp_sum_u32(u32 v) { return __reduce_add_sync(0xffffffffu, v); }
+
+// One warp per tile of 32 consecutive nodes, one sweep per launch:
+//   * coalesced load of F and of the row offsets of the tile;
+//   * selected nodes take their fluid with an atomic exchange, so pushes of
+//     other warps that race with the selection are never lost (they are
+//     either taken now or stay in F for the next sweep: conservation is exact,
+//     PAPER Theorem 3.1 holds for any split of the fluid);
+//   * the fluid-to-history swap happens in registers (H += sent);
+//   * non-hub rows are expanded edge-per-lane over the tile's contiguous
+//     column range (dense tiles) or row by row (sparse tiles), with
+//     SW_UNROLL independent column loads in flight per lane, then
+//     red.global.add of sent*d/deg into F;
+//   * hub rows (deg >= t2) are queued for the block-per-node kernel.
+template <typename FT>
+__global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
+    __shared__ double red_sm[SW_NT / 32];
+    __shared__ u64 red_sm64[SW_NT / 32];
+    __shared__ FT hot_acc[HOT_SLOTS];
+    constexpr u32 FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const SolveCtl *c = a.ctl;
+    const double theta = c->theta;
+    const u64 sweep = c->sweeps;
+    const double keep_frac = 1.0 - a.d;
+    double absorbed = 0.0, mx = 0.0;
+    u64 steps = 0, nsel = 0;
+    const long long ntiles = (a.n + 31) >> 5;
+    const long long nwarps = (long long)gridDim.x * (SW_NT / 32);
+    const u32 *__restrict__ tgt = a.tgt;
+    FT *__restrict__ F = a.F;
+    hot_clear(hot_acc, a.nhot, SW_NT);
+    __syncthreads();
+    for (long long tile = blockIdx.x * (long long)(SW_NT / 32) + (threadIdx.x >> 5); tile < ntiles; tile += nwarps) {
+        const long long base = tile << 5;
+        const long long i = base + lane;
+        const bool valid = i < a.n;
+        const long long ic = valid ? i : a.n;
+        const u64 lo = a.off[ic];
+        u64 hi = __shfl_down_sync(FULL, lo, 1);
+        if (lane == 31) hi = a.off[base + 32 < a.n ? base + 32 : a.n];
+        const u32 deg = (u32)(hi - lo);
+        const FT f = valid ? F[i] : (FT)0;
+        const double af = fabs((double)f);
+        const double score = (a.weight && valid) ? af * a.weight[i] : af;
+        mx = fmax(mx, score);
+        bool sel;
+        if (a.select == FR_SELECT_PER) sel = true;
+        else if (a.select == FR_SELECT_RAND)
+            sel = (double)(hmix(((u64)a.seed << 40) ^ (sweep << 32) ^ hmix((u64)i)) >> 11) * 0x1.0p-53 < a.rand_frac;
+        else sel = score >= theta;
+        sel = sel && valid && f != (FT)0;
+        const bool big = deg >= a.t2;
+        double pv = 0.0;
+        if (sel) {
+            const FT sent = take_fluid(F + i);  // authoritative amount (>= f for non-negative fluid)
+            const double as = fabs((double)sent);
+            a.H[i] += (double)sent;
+            nsel++;
+            if (deg == 0) {
+                absorbed += as;  // dangling: all of it leaves (PAPER sec. 3.3)
+            } else {
+                absorbed += as * keep_frac;
+                steps += deg;
+                pv = (double)sent * (a.d / (double)deg);  // sent*(d/deg), engine.py:321
+            }
+        }
+        const FT pvf = (FT)pv;
+        // hubs -> block-per-node kernel
+        const bool hub = sel && big;
+        const u32 hmask = __ballot_sync(FULL, hub);
+        if (hmask) {
+            u32 hb = 0;
+            const int leader = __ffs(hmask) - 1;
+            if (lane == leader) hb = atomicAdd(&a.ctl->qcount[2], (u32)__popc(hmask));
+            hb = __shfl_sync(FULL, hb, leader);
+            if (hub) {
+                const u32 p = hb + __popc(hmask & ((1u << lane) - 1u));
+                a.qnode[2][p] = (u32)i;
+                a.qval[2][p] = pvf;
+            }
+        }
+        const bool act = sel && !big && deg > 0;
+        const u32 amask = __ballot_sync(FULL, act);
+        if (!amask) continue;
+        const u32 act_edges = warp_sum_u32(act ? deg : 0u);
+        const u32 small_edges = warp_sum_u32(big ? 0u : deg);
+        const u64 R0 = __shfl_sync(FULL, lo, 0);
+        const u64 R1 = __shfl_sync(FULL, hi, 31);
+        if (2ull * act_edges >= small_edges && R1 - R0 < (1ull << 31)) {
+            // dense tile: walk the contiguous column range [R0, R1) edge-per-lane
+            const u32 rel = (u32)(lo - R0);
+            const u32 len = (u32)(R1 - R0);
+            u32 c0 = 0;
+            while (c0 < len) {
+                // row holding position c0 (warp-uniform); skip rows with nothing to push
+                int rf = 0;
+#pragma unroll
+                for (int s = 16; s > 0; s >>= 1) {
+                    const u32 v = __shfl_sync(FULL, rel, rf + s);
+                    if (v <= c0) rf += s;
+                }
+                if (!((amask >> rf) & 1u)) {
+                    // rf is the last row starting at or before c0, so the next row starts after c0
+                    const u32 nxt = __shfl_sync(FULL, rel, rf < 31 ? rf + 1 : 31);
+                    c0 = rf < 31 ? nxt : len;
+                    continue;
+                }
+                u32 tv[SW_UNROLL];
+                FT vv[SW_UNROLL];
+                bool ok[SW_UNROLL];
+#pragma unroll
+                for (int u = 0; u < SW_UNROLL; u++) {
+                    const u32 p = c0 + (u32)(u * 32 + lane);
+                    int r = 0;
+#pragma unroll
+                    for (int s = 16; s > 0; s >>= 1) {
+                        const u32 v = __shfl_sync(FULL, rel, r + s);
+                        if (v <= p) r += s;
+                    }
+                    ok[u] = p < len && ((amask >> r) & 1u);
+                    vv[u] = __shfl_sync(FULL, pvf, r);
+                    tv[u] = ok[u] ? __ldg(tgt + R0 + p) : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < SW_UNROLL; u++)
+                    if (ok[u]) push_one(F, hot_acc, tv[u], vv[u]);
+                c0 += 32 * SW_UNROLL;
+            }
+        } else {
+            // sparse tile: row by row, lanes over each row's columns
+            u32 m = amask;
+            while (m) {
+                const int r = __ffs(m) - 1;
+                m &= m - 1;
+                const u64 rlo = __shfl_sync(FULL, lo, r);
+                const u32 rdeg = __shfl_sync(FULL, deg, r);
+                const FT v = __shfl_sync(FULL, pvf, r);
+                for (u32 k = lane; k < rdeg; k += 32) push_one(F, hot_acc, __ldg(tgt + rlo + k), v);
+            }
+        }
+    }
+    __syncthreads();
+    hot_flush(F, hot_acc, a.slot_node, a.nhot, SW_NT);
+    const double ba = block_sum<SW_NT>(absorbed, red_sm);
+    const double bx = block_max<SW_NT>(mx, red_sm);
+    const u64 bs = block_sum_u64<SW_NT>(steps, red_sm64);
+    const u64 bn = block_sum_u64<SW_NT>(nsel, red_sm64);
+    if (threadIdx.x == 0) {
+        a.part_abs[blockIdx.x] = ba;
+        a.part_max[blockIdx.x] = bx;
+        a.part_steps[blockIdx.x] = bs;
+        a.part_sel[blockIdx.x] = bn;
+        a.part_mass[blockIdx.x] = 0.0;
     }
 }
 
@@ -284,12 +508,14 @@ template <typename FT>
 __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
     __shared__ __align__(128) u32 stage[BLK_STAGES][BLK_CHUNK];
     __shared__ __align__(8) u64 bar[BLK_STAGES];
+    __shared__ FT hot_acc[HOT_SLOTS];
     const u32 cnt = a.ctl->qcount[2];
     if (blockIdx.x >= cnt) return;
     if (threadIdx.x == 0) {
         for (int s = 0; s < BLK_STAGES; s++) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    hot_clear(hot_acc, a.nhot, BLK_NT);
     __syncthreads();
     u32 seq = 0;  // chunks consumed by this block so far (slot = seq % STAGES, parity = (seq / STAGES) & 1)
     for (u32 e = blockIdx.x; e < cnt; e += gridDim.x) {
@@ -298,8 +524,8 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
         const u64 lo = a.off[node], hi = a.off[node + 1];
         const u64 a0 = min(hi, (lo + 3) & ~3ull);
         const u64 a1 = max(a0, hi & ~3ull);
-        if (lo + threadIdx.x < a0) red_add(a.F + __ldg(a.tgt + lo + threadIdx.x), v);
-        if (a1 + threadIdx.x < hi) red_add(a.F + __ldg(a.tgt + a1 + threadIdx.x), v);
+        if (lo + threadIdx.x < a0) push_one(a.F, hot_acc, __ldg(a.tgt + lo + threadIdx.x), v);
+        if (a1 + threadIdx.x < hi) push_one(a.F, hot_acc, __ldg(a.tgt + a1 + threadIdx.x), v);
         const u64 body = a1 - a0;
         const u32 nch = (u32)((body + BLK_CHUNK - 1) / BLK_CHUNK);
         if (threadIdx.x == 0) {
@@ -323,11 +549,13 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
             const u32 len = (u32)min((u64)BLK_CHUNK, body - (u64)c * BLK_CHUNK);
             const u32 *sp = stage[s];
 #pragma unroll 4
-            for (u32 k = threadIdx.x; k < len; k += BLK_NT) red_add(a.F + sp[k], v);
+            for (u32 k = threadIdx.x; k < len; k += BLK_NT) push_one(a.F, hot_acc, sp[k], v);
             __syncthreads();  // slot s is free for the next bulk load
         }
         seq += nch;
     }
+    __syncthreads();
+    hot_flush(a.F, hot_acc, a.slot_node, a.nhot, BLK_NT);
 }
 
 // ------------------------------------------------------------------ F: finalize
@@ -351,7 +579,11 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
     nsel = block_sum_u64<FIN_NT>(nsel, sm64);
     if (threadIdx.x != 0) return;
     SolveCtl *c = a.ctl;
-    const double residual = nsel ? mass - ab : mass;
+    // binned path: the select pass saw F before any push of this sweep, so its
+    // mass is exact; fused path: pushes race with the scan, so the residual is
+    // carried incrementally like the reference's R (engine.py:322-325) and
+    // re-derived exactly by k_mass_check before the loop may stop.
+    const double residual = a.path == PATH_FUSED ? c->residual - ab : (nsel ? mass - ab : mass);
     const double theta_used = c->theta;
     c->residual = residual;
     c->diffusions += nsel;
@@ -380,10 +612,57 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
         while (th > mx) th *= a.decay;
     c->theta = th;
     c->qcount[0] = c->qcount[1] = c->qcount[2] = 0;
-    const bool done = residual <= a.thr || mass == 0.0 || (long long)c->sweeps >= a.max_sweeps ||
-                      (a.max_diffusions > 0 && (long long)c->diffusions >= a.max_diffusions);
+    const bool budget = (long long)c->sweeps >= a.max_sweeps ||
+                        (a.max_diffusions > 0 && (long long)c->diffusions >= a.max_diffusions);
+    bool done;
+    if (a.path == PATH_FUSED) {
+        // converged (by the estimate) or drained: verify with an exact sum first
+        const bool maybe = residual <= a.thr || (nsel == 0 && mx == 0.0);
+        c->need_check = maybe ? 1u : 0u;
+        done = budget;
+    } else {
+        done = budget || residual <= a.thr || mass == 0.0;
+    }
     c->stop = done ? 1u : 0u;
     if (a.in_graph) cudaGraphSetConditional(a.cond, done ? 0u : 1u);
+}
+
+// ------------------------------------------------------------------ hot-set preparation
+__global__ void k_count_ge(const long long *__restrict__ indeg, long long n, long long tau, unsigned long long *out) {
+    u64 c = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        c += indeg[i] >= tau;
+    c = warp_sum_u64(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+__global__ void k_max_ll(const long long *__restrict__ x, long long n, unsigned long long *out) {
+    long long m = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        m = x[i] > m ? x[i] : m;
+    atomicMax(out, (unsigned long long)m);
+}
+
+__global__ void k_collect_hot(const long long *__restrict__ indeg, long long n, long long tau, u32 cap,
+                              u32 *__restrict__ slot_node, u32 *__restrict__ node_slot, u32 *count) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        u32 s = 0xFFFFFFFFu;
+        if (indeg[i] >= tau) {
+            s = atomicAdd(count, 1u);
+            if (s < cap) slot_node[s] = (u32)i;
+            else s = 0xFFFFFFFFu;
+        }
+        node_slot[i] = s;
+    }
+}
+
+__global__ void k_encode_targets(const u32 *__restrict__ tgt, long long m, const u32 *__restrict__ node_slot,
+                                 u32 *__restrict__ out) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < m; k += (long long)gridDim.x * blockDim.x) {
+        const u32 t = tgt[k];
+        const u32 s = node_slot[t];
+        out[k] = s == 0xFFFFFFFFu ? t : (HOT_FLAG | s);
+    }
 }
 
 }  // namespace fr
@@ -394,13 +673,16 @@ using namespace fr;
 struct fr_solver {
     long long n, m;
     int fp32;
-    int sel_grid, thread_grid, warp_grid, block_grid;
+    int sel_grid, sweep_grid, thread_grid, warp_grid, block_grid;
+    u32 nhot;
     SolveCtl *ctl;
     fr_trace_row *trace;
     long long trace_cap;
     void *qnode_buf, *qval_buf;
     double *parts;
     u64 *parts64;
+    u32 *tgt_enc;      // fused path: column indices with hot targets encoded
+    u32 *slot_node;
     fr_solver_config cfg;
     cudaGraph_t graph;
     cudaGraphExec_t exec;
@@ -428,13 +710,16 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
     FR_CUDA(cudaGraphConditionalHandleCreate(&a.cond, s->graph, 0, 0));
     a.in_graph = 1;
     int nparts = s->sel_grid;
-    static void *dummy;
-    (void)dummy;
+    int nparts_sw = s->sweep_grid;
+    int unguarded = 0, guarded = 1;
     // prologue
     void *args_a[] = {&a};
     void *args_an[] = {&a, &nparts};
+    void *args_ans[] = {&a, &nparts_sw};
+    void *args_m0[] = {&a, &unguarded};
+    void *args_m1[] = {&a, &guarded};
     cudaGraphNode_t n_mass, n_pro, n_while;
-    FR_TRY(add_kernel<FT>(s->graph, &n_mass, nullptr, 0, (void *)k_mass_partials<FT>, s->sel_grid, SEL_NT, args_a));
+    FR_TRY(add_kernel<FT>(s->graph, &n_mass, nullptr, 0, (void *)k_mass_partials<FT>, s->sel_grid, SEL_NT, args_m0));
     FR_TRY(add_kernel<FT>(s->graph, &n_pro, &n_mass, 1, (void *)k_prologue<FT>, 1, FIN_NT, args_an));
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
@@ -443,12 +728,22 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
     cp.conditional.size = 1;
     FR_CUDA(cudaGraphAddNode(&n_while, s->graph, &n_pro, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    cudaGraphNode_t n_sel, n_p[3], n_fin;
-    FR_TRY(add_kernel<FT>(body, &n_sel, nullptr, 0, (void *)k_select<FT>, s->sel_grid, SEL_NT, args_a));
-    FR_TRY(add_kernel<FT>(body, &n_p[0], &n_sel, 1, (void *)k_push_thread<FT>, s->thread_grid, 256, args_a));
-    FR_TRY(add_kernel<FT>(body, &n_p[1], &n_sel, 1, (void *)k_push_warp<FT>, s->warp_grid, 256, args_a));
-    FR_TRY(add_kernel<FT>(body, &n_p[2], &n_sel, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
-    FR_TRY(add_kernel<FT>(body, &n_fin, n_p, 3, (void *)k_finalize<FT>, 1, FIN_NT, args_an));
+    if (a.path == PATH_FUSED) {
+        // sweep -> hub pushes -> finalize -> (guarded) exact mass -> (guarded) check
+        cudaGraphNode_t n_sw, n_hub, n_fin, n_m, n_chk;
+        FR_TRY(add_kernel<FT>(body, &n_sw, nullptr, 0, (void *)k_sweep<FT>, s->sweep_grid, SW_NT, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_hub, &n_sw, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_fin, &n_hub, 1, (void *)k_finalize<FT>, 1, FIN_NT, args_ans));
+        FR_TRY(add_kernel<FT>(body, &n_m, &n_fin, 1, (void *)k_mass_partials<FT>, s->sel_grid, SEL_NT, args_m1));
+        FR_TRY(add_kernel<FT>(body, &n_chk, &n_m, 1, (void *)k_mass_check<FT>, 1, FIN_NT, args_an));
+    } else {
+        cudaGraphNode_t n_sel, n_p[3], n_fin;
+        FR_TRY(add_kernel<FT>(body, &n_sel, nullptr, 0, (void *)k_select<FT>, s->sel_grid, SEL_NT, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_p[0], &n_sel, 1, (void *)k_push_thread<FT>, s->thread_grid, 256, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_p[1], &n_sel, 1, (void *)k_push_warp<FT>, s->warp_grid, 256, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_p[2], &n_sel, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_fin, n_p, 3, (void *)k_finalize<FT>, 1, FIN_NT, args_an));
+    }
     FR_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
     return FR_OK;
 }
@@ -458,6 +753,73 @@ static int occupancy_grid(void *func, int threads, int sms) {
     int per = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, func, threads, 0) != cudaSuccess || per < 1) per = 1;
     return per * sms;
+}
+
+// Selects up to `want` highest in-degree nodes (those with in-degree >= the
+// smallest threshold tau whose count fits) and writes the solver-private
+// encoded column indices.  Skipped when no node is hot enough to matter.
+template <typename FT>
+static int prepare_hot(fr_solver *s, SweepArgs<FT> &a, int want) {
+    if (want > HOT_SLOTS) want = HOT_SLOTS;
+    const long long n = s->n, m = s->m;
+    DeviceInfo di;
+    FR_TRY(device_info(&di));
+    cudaStream_t st = 0;
+    Scratch scratch(st);
+    long long *indeg;
+    unsigned long long *cnt;
+    FR_TRY(scratch.alloc(&indeg, (size_t)n));
+    FR_TRY(scratch.alloc(&cnt, 1));
+    FR_TRY(fr_in_degree(n, m, a.tgt, reinterpret_cast<int64_t *>(indeg), st));
+    const int g = di.sms * 8;
+    unsigned long long hmax = 0;
+    FR_CUDA(cudaMemsetAsync(cnt, 0, sizeof(*cnt), st));
+    k_max_ll<<<g, 256, 0, st>>>(indeg, n, cnt);
+    FR_CUDA(cudaMemcpyAsync(&hmax, cnt, sizeof(hmax), cudaMemcpyDeviceToHost, st));
+    FR_CUDA(cudaStreamSynchronize(st));
+    const long long min_hot = 64;  // below this a target cannot serialise a sweep
+    if ((long long)hmax < min_hot) return FR_OK;
+    // smallest tau >= min_hot with count(indeg >= tau) <= want
+    long long lo = min_hot, hi = (long long)hmax;  // count(>= hi) >= 1
+    auto count_ge = [&](long long tau, unsigned long long *out) -> int {
+        FR_CUDA(cudaMemsetAsync(cnt, 0, sizeof(*cnt), st));
+        k_count_ge<<<g, 256, 0, st>>>(indeg, n, tau, cnt);
+        FR_CUDA(cudaMemcpyAsync(out, cnt, sizeof(*out), cudaMemcpyDeviceToHost, st));
+        FR_CUDA(cudaStreamSynchronize(st));
+        return FR_OK;
+    };
+    unsigned long long c_lo = 0;
+    FR_TRY(count_ge(lo, &c_lo));
+    long long tau = lo;
+    if (c_lo > (unsigned long long)want) {
+        while (hi - lo > 1) {  // invariant: count(lo) > want
+            const long long mid = lo + (hi - lo) / 2;
+            unsigned long long c;
+            FR_TRY(count_ge(mid, &c));
+            if (c > (unsigned long long)want) lo = mid; else hi = mid;
+        }
+        tau = hi;
+    }
+    u32 *node_slot, *d_count;
+    FR_TRY(scratch.alloc(&node_slot, (size_t)n));
+    FR_TRY(scratch.alloc(&d_count, 1));
+    FR_CUDA(cudaMalloc(&s->slot_node, sizeof(u32) * HOT_SLOTS));
+    FR_CUDA(cudaMemsetAsync(d_count, 0, sizeof(u32), st));
+    k_collect_hot<<<g, 256, 0, st>>>(indeg, n, tau, (u32)want, s->slot_node, node_slot, d_count);
+    u32 nhot = 0;
+    FR_CUDA(cudaMemcpyAsync(&nhot, d_count, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    FR_CUDA(cudaStreamSynchronize(st));
+    if (nhot > (u32)want) nhot = (u32)want;
+    if (nhot == 0) return FR_OK;
+    FR_CUDA(cudaMalloc(&s->tgt_enc, sizeof(u32) * (size_t)m));
+    k_encode_targets<<<g, 256, 0, st>>>(a.tgt, m, node_slot, s->tgt_enc);
+    FR_CUDA(cudaGetLastError());
+    FR_CUDA(cudaStreamSynchronize(st));
+    a.tgt = s->tgt_enc;
+    a.slot_node = s->slot_node;
+    a.nhot = nhot;
+    s->nhot = nhot;
+    return FR_OK;
 }
 
 template <typename FT>
@@ -488,6 +850,7 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.select = c.select;
     a.policy = c.policy;
     a.seed = c.seed;
+    a.path = c.kernel_path == 1 ? PATH_BINNED : PATH_FUSED;
     // queues: a selected node lands in exactly one bin
     const long long n = s->n, m = s->m;
     const long long cap0 = n;
@@ -509,7 +872,10 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     s->thread_grid = occupancy_grid<FT>((void *)k_push_thread<FT>, 256, di.sms);
     s->warp_grid = occupancy_grid<FT>((void *)k_push_warp<FT>, 256, di.sms);
     s->block_grid = occupancy_grid<FT>((void *)k_push_block<FT>, BLK_NT, di.sms);
-    const int P = s->sel_grid;
+    s->sweep_grid = occupancy_grid<FT>((void *)k_sweep<FT>, SW_NT, di.sms);
+    const long long wtiles = ((n + 31) / 32 + SW_NT / 32 - 1) / (SW_NT / 32);
+    if (s->sweep_grid > wtiles) s->sweep_grid = (int)std::max<long long>(1, wtiles);
+    const int P = std::max(s->sel_grid, s->sweep_grid);
     FR_CUDA(cudaMalloc(&s->parts, sizeof(double) * 3 * (size_t)P));
     FR_CUDA(cudaMalloc(&s->parts64, sizeof(u64) * 2 * (size_t)P));
     a.part_mass = s->parts;
@@ -517,6 +883,9 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.part_max = s->parts + 2 * P;
     a.part_steps = s->parts64;
     a.part_sel = s->parts64 + P;
+    a.slot_node = nullptr;
+    a.nhot = 0;
+    if (a.path == PATH_FUSED && c.hot_slots >= 0 && m > 0) FR_TRY(prepare_hot(s, a, c.hot_slots ? c.hot_slots : HOT_SLOTS));
     return build_graph<FT>(s, a);
 }
 
@@ -622,9 +991,9 @@ template <typename FT>
 static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve_stats *h_stats, double *ms,
                         int64_t *launches) {
     a.in_graph = 0;
-    int nparts = s->sel_grid;
+    int nparts = s->sel_grid, nparts_sw = s->sweep_grid;
     FR_TRY(reset_ctl(s, st));
-    k_mass_partials<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a);
+    k_mass_partials<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a, 0);
     k_prologue<FT><<<1, FIN_NT, 0, st>>>(a, nparts);
     FR_CUDA(cudaGetLastError());
     cudaEvent_t ev[6];
@@ -633,17 +1002,24 @@ static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve
     u32 stop = 0;
     FR_CUDA(cudaMemcpyAsync(&stop, &s->ctl->stop, sizeof(u32), cudaMemcpyDeviceToHost, st));
     FR_CUDA(cudaStreamSynchronize(st));
+    const bool fused = a.path == PATH_FUSED;
     while (!stop) {
+        // kernel classes: 0 select/sweep, 1 thread-bin push, 2 warp-bin push, 3 block-bin push, 4 finalize
         FR_CUDA(cudaEventRecord(ev[0], st));
-        k_select<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a);
+        if (fused) k_sweep<FT><<<s->sweep_grid, SW_NT, 0, st>>>(a);
+        else k_select<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[1], st));
-        k_push_thread<FT><<<s->thread_grid, 256, 0, st>>>(a);
+        if (!fused) k_push_thread<FT><<<s->thread_grid, 256, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[2], st));
-        k_push_warp<FT><<<s->warp_grid, 256, 0, st>>>(a);
+        if (!fused) k_push_warp<FT><<<s->warp_grid, 256, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[3], st));
         k_push_block<FT><<<s->block_grid, BLK_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[4], st));
-        k_finalize<FT><<<1, FIN_NT, 0, st>>>(a, nparts);
+        k_finalize<FT><<<1, FIN_NT, 0, st>>>(a, fused ? nparts_sw : nparts);
+        if (fused) {
+            k_mass_partials<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a, 1);
+            k_mass_check<FT><<<1, FIN_NT, 0, st>>>(a, nparts);
+        }
         FR_CUDA(cudaEventRecord(ev[5], st));
         FR_CUDA(cudaGetLastError());
         FR_CUDA(cudaMemcpyAsync(&stop, &s->ctl->stop, sizeof(u32), cudaMemcpyDeviceToHost, st));
@@ -652,7 +1028,7 @@ static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve
             float t = 0.f;
             FR_CUDA(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
             ms[k] += t;
-            launches[k] += 1;
+            if (fused ? (k == 0 || k >= 3) : true) launches[k] += 1;
         }
     }
     for (int i = 0; i < 6; i++) cudaEventDestroy(ev[i]);
@@ -699,6 +1075,8 @@ extern "C" int fr_solver_destroy(fr_solver *s) {
     cudaFree(s->qval_buf);
     cudaFree(s->parts);
     cudaFree(s->parts64);
+    cudaFree(s->tgt_enc);
+    cudaFree(s->slot_node);
     delete s;
     return FR_OK;
 }

@@ -32,7 +32,7 @@ class DeviceSchedule:
     """A selection rule plus its theta policy; consumed by engine.run."""
 
     def __init__(self, kind, seed=0, decay=0.5, policy="exhaust", rand_frac=0.25,
-                 mass_frac=0.5, thread_max_degree=0, block_min_degree=0):
+                 mass_frac=0.5, thread_max_degree=0, block_min_degree=0, kernel_path="fused", hot_slots=0):
         if kind not in KINDS:
             raise ValueError(f"unknown scheduler kind {kind!r}; expected one of {KINDS}")
         if not 0.0 < decay < 1.0:
@@ -47,6 +47,10 @@ class DeviceSchedule:
         self.mass_frac = float(mass_frac)
         self.thread_max_degree = int(thread_max_degree)
         self.block_min_degree = int(block_min_degree)
+        if kernel_path not in ("fused", "binned"):
+            raise ValueError(f"kernel_path must be 'fused' or 'binned', got {kernel_path!r}")
+        self.kernel_path = kernel_path
+        self.hot_slots = int(hot_slots)
         self._per_count = 0
         self._rng = None
 
@@ -76,6 +80,8 @@ class DeviceSchedule:
         c.thread_max_degree = self.thread_max_degree
         c.block_min_degree = self.block_min_degree
         c.seed = self.seed & 0xFFFFFFFF
+        c.kernel_path = 0 if self.kernel_path == "fused" else 1
+        c.hot_slots = self.hot_slots
         return c
 
     # -- reference single-node interface -------------------------------

@@ -26,14 +26,15 @@ def l1(a, b):
     return float(np.abs(a - b).sum())
 
 
+@pytest.mark.parametrize("path", ["fused", "binned"])
 @pytest.mark.parametrize("kind", KINDS)
-def test_small_graphs_match_reference(cuda, golden_small, oracle, kind):
+def test_small_graphs_match_reference(cuda, golden_small, oracle, kind, path):
     for tag in golden_small["tags"]:
         tag = str(tag)
         g = graph_from(cuda, golden_small[f"{tag}_off"], golden_small[f"{tag}_tgt"])
         tel = golden_small[f"{tag}_teleport"] if f"{tag}_teleport" in golden_small else None
         params = cuda.DiffusionParams(damping=0.85, teleport=tel, target_error=1e-11)
-        rank, trace = cuda.run(g, params, cuda.make_scheduler(kind, seed=3))
+        rank, trace = cuda.run(g, params, cuda.make_scheduler(kind, seed=3, kernel_path=path))
         # the reference's own rank at a tight target (the oracle is bit-exact with it,
         # test_oracle_golden.py); the goldens themselves were taken at 1e-9..1e-10
         truth = oracle.run_seq(golden_small[f"{tag}_off"], golden_small[f"{tag}_tgt"], 0.85, 1e-14,
@@ -46,12 +47,13 @@ def test_small_graphs_match_reference(cuda, golden_small, oracle, kind):
         assert trace.rows[-1].residual <= 1e-11 * 0.15
 
 
-def test_config1_matches_reference(cuda, golden_configs):
+@pytest.mark.parametrize("path", ["fused", "binned"])
+def test_config1_matches_reference(cuda, golden_configs, path):
     """BASELINE config 1: 10k uniform graph, residual < 1e-10, fp64."""
     g = graph_from(cuda, golden_configs["cfg1_off"], golden_configs["cfg1_tgt"])
-    for policy in ("exhaust", "geometric"):
+    for policy, decay in (("exhaust", 0.5), ("geometric", 0.5), ("geometric", 0.9)):
         rank, trace = cuda.run(g, cuda.DiffusionParams(target_error=1e-10),
-                               cuda.make_scheduler("sweep", policy=policy))
+                               cuda.make_scheduler("sweep", policy=policy, sweep_decay=decay, kernel_path=path))
         assert l1(rank, golden_configs["cfg1_sweep_rank"]) <= L1_FP64
         assert trace.rows[-1].residual <= 1e-10 * 0.15
 
@@ -71,18 +73,19 @@ def test_sweep_counters_match_parallel_oracle(cuda, oracle):
         ref = oracle.run_psweep(off, tgt, 0.85, 1e-10, policy=code)
         state = cuda.init(g, cuda.DiffusionParams(target_error=1e-10))
         rank, trace = cuda.run(g, cuda.DiffusionParams(target_error=1e-10),
-                               cuda.make_scheduler("sweep", policy=policy), state=state)
+                               cuda.make_scheduler("sweep", policy=policy, kernel_path="binned"), state=state)
         assert l1(rank, ref.rank) <= 2e-10
         # the selected sets can differ only through last-bit rounding near theta
         assert abs(state.sweeps - ref.sweeps) <= max(2, ref.sweeps // 50)
         assert abs(state.elementary_steps - ref.elementary_steps) <= 0.02 * ref.elementary_steps
 
 
-def test_fp32_fluid_variant(cuda, golden_configs):
+@pytest.mark.parametrize("path", ["fused", "binned"])
+def test_fp32_fluid_variant(cuda, golden_configs, path):
     """fp32 fluid / fp64 history: stated tolerance 1e-6 L1 against the fp64 reference."""
     g = graph_from(cuda, golden_configs["web5k_off"], golden_configs["web5k_tgt"])
-    rank, trace = cuda.run(g, cuda.DiffusionParams(target_error=1e-9), cuda.make_scheduler("sweep"),
-                           fluid_dtype=torch.float32)
+    rank, trace = cuda.run(g, cuda.DiffusionParams(target_error=1e-9),
+                           cuda.make_scheduler("sweep", kernel_path=path), fluid_dtype=torch.float32)
     assert l1(rank, golden_configs["web5k_sweep_rank"]) <= 1e-6
 
 
@@ -142,7 +145,8 @@ def test_conservation_identity_mid_run(cuda, oracle):
     params = cuda.DiffusionParams(target_error=1e-12)
     state = cuda.init(g, params)
     f0 = state.fluid.cpu().numpy().copy()
-    cuda.run(g, params, cuda.make_scheduler("sweep"), state=state, max_sweeps=7)
+    cuda.run(g, params, cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9), state=state, max_sweeps=7)
+    torch.cuda.synchronize()
     h = state.history.cpu().numpy()
     f = state.fluid.cpu().numpy()
     deg = np.diff(off)
@@ -151,6 +155,8 @@ def test_conservation_identity_mid_run(cuda, oracle):
     np.add.at(push, tgt.astype(np.int64), h[src_e] / deg[src_e])
     assert np.abs(h + f - f0 - 0.85 * push).max() <= 1e-15
     assert state.sweeps == 7
+    # the fused kernel's exact fluid mass equals the run's residual bookkeeping
+    assert abs(f.sum() - state.residual) <= 1e-15
 
 
 def test_bound_equals_true_error_without_dangling(cuda):
@@ -217,3 +223,18 @@ def test_host_buffer_entry_point(cuda, golden_configs):
     _lib.check(_lib.lib.fr_pagerank_host(n, tgt.size, off.ctypes.data, tgt.ctypes.data, ctypes.byref(cfg),
                                          rank.ctypes.data, ctypes.byref(stats)))
     assert l1(rank, golden_configs["cfg1_sweep_rank"]) <= L1_FP64
+
+
+@pytest.mark.parametrize("hot_slots", [-1, 0, 7])
+def test_hot_slot_aggregation(cuda, oracle, hot_slots):
+    """Shared-memory aggregation of pushes into in-degree hubs keeps exact conservation."""
+    src, dst = oracle.gen_edges(oracle.web_config(8.0), 200_000, 31)
+    off, tgt, _ = oracle.csr_build(200_000, src, dst, clean=True)
+    g = graph_from(cuda, off, tgt)
+    params = cuda.DiffusionParams(target_error=1e-10)
+    sched = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9, hot_slots=hot_slots)
+    state = cuda.init(g, params)
+    rank, trace = cuda.run(g, params, sched, state=state)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-11, "sweep").rank
+    assert l1(rank, ref) <= 2e-10
+    assert state.residual <= 1e-10 * 0.15
