@@ -248,7 +248,8 @@ def run_ours(args, world, rank, local):
     params = fr.DiffusionParams(damping=w["damping"], target_error=w["target"])
     sched = fr.make_scheduler("sweep", policy=args.policy, sweep_decay=args.decay,
                               thread_max_degree=args.thread_max, block_min_degree=args.block_min,
-                              kernel_path=args.path, hot_slots=args.hot_slots)
+                              kernel_path=args.path, hot_slots=args.hot_slots,
+                              warm_slots=args.warm_slots)
     state = fr.init(g, params, fluid_dtype=torch.float32 if fp32 else torch.float64)
     solver = fr.Solver(g, state, sched, params, trace_cap=1 << 16)
     rank_out = torch.empty(n, dtype=torch.float64, device=dev)
@@ -363,7 +364,7 @@ def run_ours(args, world, rank, local):
             "config": {"workload": w["name"], "n": n, "edges": L, "edge_slots_drawn": slots,
                        "duplicates_dropped": dups, "self_loops_dropped": loops, "damping": w["damping"],
                        "target_error": w["target"], "policy": args.policy, "decay": args.decay,
-                       "kernel_path": args.path, "hot_slots": args.hot_slots,
+                       "kernel_path": args.path, "hot_slots": args.hot_slots, "warm_slots": args.warm_slots,
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (CSR %.1f GB >> 126 MB)" % ((8 * (n + 1) + 4 * L) / 1e9)},
             "time_to_residual_s": ms_per_step / 1000.0,
@@ -398,6 +399,7 @@ def main():
     ap.add_argument("--decay", type=float, default=0.9)
     ap.add_argument("--path", default="fused", choices=("fused", "binned"))
     ap.add_argument("--hot-slots", type=int, default=0, help="0 default (2048), -1 off")
+    ap.add_argument("--warm-slots", type=int, default=0, help="0 default (2^21), -1 off")
     ap.add_argument("--fluid", default="fp64", choices=("fp64", "fp32"))
     ap.add_argument("--thread-max", type=int, default=0)
     ap.add_argument("--block-min", type=int, default=0)

@@ -142,6 +142,10 @@ typedef struct fr_solver_config {
     int32_t hot_slots;        /* fused path: pushes into the hot_slots highest in-degree
                                  nodes are summed per block in shared memory first
                                  (0 = default 2048, max 2048; -1 = off)             */
+    int32_t warm_slots;       /* fused path: pushes into the next warm_slots highest
+                                 in-degree nodes go to a compact L2-resident array that
+                                 is folded back into F after every sweep
+                                 (0 = default 2^21, -1 = off)                       */
 } fr_solver_config;
 
 typedef struct fr_trace_row {

@@ -23,6 +23,9 @@
 // The sweep loop is a CUDA-graph while-node: the host launches one graph per
 // solve and waits once; there is no per-sweep host round trip.
 #include <math.h>
+#include <stdlib.h>
+
+#include <climits>
 
 #include <algorithm>
 #include <vector>
@@ -50,6 +53,7 @@ struct SolveCtl {
     u32 stop;
     u32 need_check;     // fused path: incremental residual crossed the target, verify exactly
     u32 pad;
+    u64 seg_next[16];   // fused path: in-order tile counters, one per node segment
 };
 
 enum { PATH_FUSED = 0, PATH_BINNED = 1 };
@@ -66,8 +70,10 @@ struct SweepArgs {
     FT *qval[3];
     double *part_mass, *part_abs, *part_max;
     u64 *part_steps, *part_sel;
-    const u32 *slot_node;  // hot slot -> node (fused path)
-    u32 nhot;
+    const u32 *slot_node;  // slot -> node for the hot and warm classes (fused path)
+    FT *Fw;                // compact fluid of the slotted nodes, folded into F every sweep
+    u32 nhot;              // slots [0, nhot): shared-memory aggregated
+    u32 nslots;            // slots [nhot, nslots): red.add into the L2-resident Fw
     fr_trace_row *trace;
     long long n;
     long long trace_cap;
@@ -126,6 +132,7 @@ __global__ void __launch_bounds__(FIN_NT) k_prologue(SweepArgs<FT> a, int nparts
         c->residual = mass;
         c->mass0 = mass;
         c->qcount[0] = c->qcount[1] = c->qcount[2] = 0;
+        for (int q = 0; q < 16; q++) c->seg_next[q] = 0;
         c->stop = (mass <= a.thr || mass == 0.0) ? 1u : 0u;
         if (a.in_graph) cudaGraphSetConditional(a.cond, c->stop ? 0u : 1u);
     }
@@ -158,12 +165,19 @@ __global__ void __launch_bounds__(FIN_NT) k_mass_check(SweepArgs<FT> a, int npar
 // keeps a private copy of the column indices in which such targets carry
 // HOT_FLAG | slot (slot_node[slot] = node id).
 static constexpr int HOT_SLOTS = 2048;
+static constexpr u32 WARM_SLOTS = 2u << 20;  // 16 MB of fp64 fluid
 static constexpr u32 HOT_FLAG = 0x80000000u;
 
 template <typename FT>
-__device__ __forceinline__ void push_one(FT *__restrict__ F, FT *hot_acc, u32 t, FT v) {
-    if (t & HOT_FLAG) atomicAdd(hot_acc + (t & ~HOT_FLAG), v);  // shared memory
-    else red_add(F + t, v);
+__device__ __forceinline__ void push_one(FT *__restrict__ F, FT *__restrict__ Fw, FT *hot_acc, u32 nhot, u32 t,
+                                         FT v) {
+    if (t & HOT_FLAG) {
+        const u32 sl = t & ~HOT_FLAG;
+        if (sl < nhot) atomicAdd(hot_acc + sl, v);  // shared memory
+        else red_add(Fw + sl, v);                  // compact, L2-resident
+    } else {
+        red_add(F + t, v);
+    }
 }
 
 template <typename FT>
@@ -172,17 +186,31 @@ __device__ __forceinline__ void hot_clear(FT *hot_acc, u32 nhot, int nt) {
 }
 
 template <typename FT>
-__device__ __forceinline__ void hot_flush(FT *__restrict__ F, const FT *hot_acc, const u32 *__restrict__ slot_node,
-                                          u32 nhot, int nt) {
+__device__ __forceinline__ void hot_flush(FT *__restrict__ Fw, const FT *hot_acc, u32 nhot, int nt) {
     for (u32 s = threadIdx.x; s < nhot; s += nt) {
         const FT x = hot_acc[s];
-        if (x != (FT)0) red_add(F + slot_node[s], x);
+        if (x != (FT)0) red_add(Fw + s, x);
+    }
+}
+
+// Moves the fluid gathered in Fw back to the slotted nodes (runs alone, after
+// every push of the sweep), so F is complete when the next sweep starts.
+template <typename FT>
+__global__ void __launch_bounds__(256) k_fold(SweepArgs<FT> a) {
+    for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < a.nslots; s += gridDim.x * blockDim.x) {
+        const FT v = a.Fw[s];
+        if (v != (FT)0) {
+            a.F[a.slot_node[s]] += v;
+            a.Fw[s] = (FT)0;
+        }
     }
 }
 
 // ------------------------------------------------------------------ fused sweep (default path)
 static constexpr int SW_NT = 256;
 static constexpr int SW_UNROLL = 4;
+static constexpr int SW_SEGS = 16;
+static constexpr int SW_CHUNK = 8;
 
 __device__ __forceinline__ double take_fluid(double *p) {
     return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
@@ -217,21 +245,66 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
     double absorbed = 0.0, mx = 0.0;
     u64 steps = 0, nsel = 0;
     const long long ntiles = (a.n + 31) >> 5;
-    const long long nwarps = (long long)gridDim.x * (SW_NT / 32);
     const u32 *__restrict__ tgt = a.tgt;
     FT *__restrict__ F = a.F;
     hot_clear(hot_acc, a.nhot, SW_NT);
     __syncthreads();
-    for (long long tile = blockIdx.x * (long long)(SW_NT / 32) + (threadIdx.x >> 5); tile < ntiles; tile += nwarps) {
-        const long long base = tile << 5;
-        const long long i = base + lane;
+    // In-order scheduling: the tiles are split into SW_SEGS contiguous segments,
+    // each with its own counter; a warp takes SW_CHUNK consecutive tiles of its
+    // segment at a time and moves on to the next segment when its own is done.
+    // Every segment therefore has one tight moving front, so the fluid lines
+    // that neighbouring sources push into (local targets) are hit while they
+    // are still in L2 instead of being refilled (tools/red_probe.cu: in-order
+    // chunks reach the minimum DRAM traffic, free-running warps ~1.8x it).
+    const long long seg_tiles = (ntiles + SW_SEGS - 1) / SW_SEGS;
+    int seg = (int)((blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5)) % SW_SEGS), misses = 0;
+    long long chunk_end = 0;
+    auto grab = [&](long long &t) -> bool {
+        while (misses < SW_SEGS) {
+            unsigned long long k = 0;
+            if (lane == 0) k = atomicAdd(&a.ctl->seg_next[seg], (unsigned long long)SW_CHUNK);
+            k = __shfl_sync(FULL, k, 0);
+            const long long s0 = (long long)seg * seg_tiles;
+            const long long s1 = s0 + seg_tiles < ntiles ? s0 + seg_tiles : ntiles;
+            if (s0 + (long long)k < s1) {
+                t = s0 + (long long)k;
+                chunk_end = t + SW_CHUNK < s1 ? t + SW_CHUNK : s1;
+                misses = 0;
+                return true;
+            }
+            seg = (seg + 1) % SW_SEGS;
+            misses++;
+        }
+        return false;
+    };
+    long long tile = 0;
+    bool have = grab(tile);
+    // software pipeline: fluid and row offsets of the next tile are in flight
+    // while the current tile is processed
+    FT f_cur = (FT)0;
+    u64 lo_cur = 0, end_cur = 0;
+    auto load_tile = [&](long long t, FT &fo, u64 &loo, u64 &endo) {
+        const long long b = t << 5, i = b + lane;
+        const bool v = i < a.n;
+        loo = a.off[v ? i : a.n];
+        endo = lane == 31 ? a.off[b + 32 < a.n ? b + 32 : a.n] : 0ull;
+        fo = v ? F[i] : (FT)0;
+    };
+    if (have) load_tile(tile, f_cur, lo_cur, end_cur);
+    while (have) {
+        long long nxt = tile + 1;
+        const bool have_nx = nxt < chunk_end ? true : grab(nxt);
+        FT f_nx = (FT)0;
+        u64 lo_nx = 0, end_nx = 0;
+        if (have_nx) load_tile(nxt, f_nx, lo_nx, end_nx);
+
+        const long long i = (tile << 5) + lane;
         const bool valid = i < a.n;
-        const long long ic = valid ? i : a.n;
-        const u64 lo = a.off[ic];
+        const u64 lo = lo_cur;
         u64 hi = __shfl_down_sync(FULL, lo, 1);
-        if (lane == 31) hi = a.off[base + 32 < a.n ? base + 32 : a.n];
+        if (lane == 31) hi = end_cur;
         const u32 deg = (u32)(hi - lo);
-        const FT f = valid ? F[i] : (FT)0;
+        const FT f = f_cur;
         const double af = fabs((double)f);
         const double score = (a.weight && valid) ? af * a.weight[i] : af;
         mx = fmax(mx, score);
@@ -242,11 +315,49 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
         else sel = score >= theta;
         sel = sel && valid && f != (FT)0;
         const bool big = deg >= a.t2;
+        const bool act = sel && !big && deg > 0;
+        // take the fluid (authoritative amount, >= f for non-negative fluid) and
+        // fetch H; both are in flight while the first column loads are issued
+        FT sent = (FT)0;
+        double h_old = 0.0;
+        if (sel) {
+            sent = take_fluid(F + i);
+            h_old = a.H[i];
+        }
+        // compacted edge space of the active rows of this tile
+        const u32 adeg = act ? deg : 0u;
+        u32 incl = adeg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const u32 start = incl - adeg;
+        const u32 total = __shfl_sync(FULL, incl, 31);
+        u32 tv[2][SW_UNROLL];
+        int rv[2][SW_UNROLL];
+        auto issue = [&](int buf, u32 c0) {
+#pragma unroll
+            for (int u = 0; u < SW_UNROLL; u++) {
+                const u32 p = c0 + (u32)(u * 32 + lane);
+                int r = 0;
+#pragma unroll
+                for (int s2 = 16; s2 > 0; s2 >>= 1) {
+                    const u32 v = __shfl_sync(FULL, start, r + s2);
+                    if (v <= p) r += s2;
+                }
+                const u64 rlo = __shfl_sync(FULL, lo, r);
+                const u32 rs = __shfl_sync(FULL, start, r);
+                rv[buf][u] = p < total ? r : -1;
+                tv[buf][u] = p < total ? __ldg(tgt + rlo + (p - rs)) : 0u;
+            }
+        };
+        if (total) issue(0, 0);
+        // fluid-to-history swap in registers, push value, counters
         double pv = 0.0;
         if (sel) {
-            const FT sent = take_fluid(F + i);  // authoritative amount (>= f for non-negative fluid)
             const double as = fabs((double)sent);
-            a.H[i] += (double)sent;
+            a.H[i] = h_old + (double)sent;
             nsel++;
             if (deg == 0) {
                 absorbed += as;  // dangling: all of it leaves (PAPER sec. 3.3)
@@ -266,73 +377,31 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
             if (lane == leader) hb = atomicAdd(&a.ctl->qcount[2], (u32)__popc(hmask));
             hb = __shfl_sync(FULL, hb, leader);
             if (hub) {
-                const u32 p = hb + __popc(hmask & ((1u << lane) - 1u));
-                a.qnode[2][p] = (u32)i;
-                a.qval[2][p] = pvf;
+                const u32 q = hb + __popc(hmask & ((1u << lane) - 1u));
+                a.qnode[2][q] = (u32)i;
+                a.qval[2][q] = pvf;
             }
         }
-        const bool act = sel && !big && deg > 0;
-        const u32 amask = __ballot_sync(FULL, act);
-        if (!amask) continue;
-        const u32 act_edges = warp_sum_u32(act ? deg : 0u);
-        const u32 small_edges = warp_sum_u32(big ? 0u : deg);
-        const u64 R0 = __shfl_sync(FULL, lo, 0);
-        const u64 R1 = __shfl_sync(FULL, hi, 31);
-        if (2ull * act_edges >= small_edges && R1 - R0 < (1ull << 31)) {
-            // dense tile: walk the contiguous column range [R0, R1) edge-per-lane
-            const u32 rel = (u32)(lo - R0);
-            const u32 len = (u32)(R1 - R0);
-            u32 c0 = 0;
-            while (c0 < len) {
-                // row holding position c0 (warp-uniform); skip rows with nothing to push
-                int rf = 0;
+        // scatter, one batch of 32*SW_UNROLL edges in flight ahead of the reds
+        int buf = 0;
+        for (u32 c0 = 0; c0 < total; c0 += 32 * SW_UNROLL) {
+            if (c0 + 32 * SW_UNROLL < total) issue(buf ^ 1, c0 + 32 * SW_UNROLL);
 #pragma unroll
-                for (int s = 16; s > 0; s >>= 1) {
-                    const u32 v = __shfl_sync(FULL, rel, rf + s);
-                    if (v <= c0) rf += s;
-                }
-                if (!((amask >> rf) & 1u)) {
-                    // rf is the last row starting at or before c0, so the next row starts after c0
-                    const u32 nxt = __shfl_sync(FULL, rel, rf < 31 ? rf + 1 : 31);
-                    c0 = rf < 31 ? nxt : len;
-                    continue;
-                }
-                u32 tv[SW_UNROLL];
-                FT vv[SW_UNROLL];
-                bool ok[SW_UNROLL];
-#pragma unroll
-                for (int u = 0; u < SW_UNROLL; u++) {
-                    const u32 p = c0 + (u32)(u * 32 + lane);
-                    int r = 0;
-#pragma unroll
-                    for (int s = 16; s > 0; s >>= 1) {
-                        const u32 v = __shfl_sync(FULL, rel, r + s);
-                        if (v <= p) r += s;
-                    }
-                    ok[u] = p < len && ((amask >> r) & 1u);
-                    vv[u] = __shfl_sync(FULL, pvf, r);
-                    tv[u] = ok[u] ? __ldg(tgt + R0 + p) : 0u;
-                }
-#pragma unroll
-                for (int u = 0; u < SW_UNROLL; u++)
-                    if (ok[u]) push_one(F, hot_acc, tv[u], vv[u]);
-                c0 += 32 * SW_UNROLL;
+            for (int u = 0; u < SW_UNROLL; u++) {
+                const int r = rv[buf][u];
+                const FT v = __shfl_sync(FULL, pvf, r < 0 ? 0 : r);
+                if (r >= 0) push_one(F, a.Fw, hot_acc, a.nhot, tv[buf][u], v);
             }
-        } else {
-            // sparse tile: row by row, lanes over each row's columns
-            u32 m = amask;
-            while (m) {
-                const int r = __ffs(m) - 1;
-                m &= m - 1;
-                const u64 rlo = __shfl_sync(FULL, lo, r);
-                const u32 rdeg = __shfl_sync(FULL, deg, r);
-                const FT v = __shfl_sync(FULL, pvf, r);
-                for (u32 k = lane; k < rdeg; k += 32) push_one(F, hot_acc, __ldg(tgt + rlo + k), v);
-            }
+            buf ^= 1;
         }
+        f_cur = f_nx;
+        lo_cur = lo_nx;
+        end_cur = end_nx;
+        tile = nxt;
+        have = have_nx;
     }
     __syncthreads();
-    hot_flush(F, hot_acc, a.slot_node, a.nhot, SW_NT);
+    hot_flush(a.Fw, hot_acc, a.nhot, SW_NT);
     const double ba = block_sum<SW_NT>(absorbed, red_sm);
     const double bx = block_max<SW_NT>(mx, red_sm);
     const u64 bs = block_sum_u64<SW_NT>(steps, red_sm64);
@@ -524,8 +593,8 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
         const u64 lo = a.off[node], hi = a.off[node + 1];
         const u64 a0 = min(hi, (lo + 3) & ~3ull);
         const u64 a1 = max(a0, hi & ~3ull);
-        if (lo + threadIdx.x < a0) push_one(a.F, hot_acc, __ldg(a.tgt + lo + threadIdx.x), v);
-        if (a1 + threadIdx.x < hi) push_one(a.F, hot_acc, __ldg(a.tgt + a1 + threadIdx.x), v);
+        if (lo + threadIdx.x < a0) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + lo + threadIdx.x), v);
+        if (a1 + threadIdx.x < hi) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + a1 + threadIdx.x), v);
         const u64 body = a1 - a0;
         const u32 nch = (u32)((body + BLK_CHUNK - 1) / BLK_CHUNK);
         if (threadIdx.x == 0) {
@@ -549,13 +618,13 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
             const u32 len = (u32)min((u64)BLK_CHUNK, body - (u64)c * BLK_CHUNK);
             const u32 *sp = stage[s];
 #pragma unroll 4
-            for (u32 k = threadIdx.x; k < len; k += BLK_NT) push_one(a.F, hot_acc, sp[k], v);
+            for (u32 k = threadIdx.x; k < len; k += BLK_NT) push_one(a.F, a.Fw, hot_acc, a.nhot, sp[k], v);
             __syncthreads();  // slot s is free for the next bulk load
         }
         seq += nch;
     }
     __syncthreads();
-    hot_flush(a.F, hot_acc, a.slot_node, a.nhot, BLK_NT);
+    hot_flush(a.Fw, hot_acc, a.nhot, BLK_NT);
 }
 
 // ------------------------------------------------------------------ F: finalize
@@ -612,6 +681,7 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
         while (th > mx) th *= a.decay;
     c->theta = th;
     c->qcount[0] = c->qcount[1] = c->qcount[2] = 0;
+    for (int q = 0; q < 16; q++) c->seg_next[q] = 0;
     const bool budget = (long long)c->sweeps >= a.max_sweeps ||
                         (a.max_diffusions > 0 && (long long)c->diffusions >= a.max_diffusions);
     bool done;
@@ -643,16 +713,19 @@ __global__ void k_max_ll(const long long *__restrict__ x, long long n, unsigned 
     atomicMax(out, (unsigned long long)m);
 }
 
-__global__ void k_collect_hot(const long long *__restrict__ indeg, long long n, long long tau, u32 cap,
-                              u32 *__restrict__ slot_node, u32 *__restrict__ node_slot, u32 *count) {
+// Nodes with tau_lo <= in-degree < tau_hi get slots base, base+1, ... (< base+cap).
+__global__ void k_collect_class(const long long *__restrict__ indeg, long long n, long long tau_lo, long long tau_hi,
+                                u32 base, u32 cap, u32 *__restrict__ slot_node, u32 *__restrict__ node_slot,
+                                u32 *count) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        u32 s = 0xFFFFFFFFu;
-        if (indeg[i] >= tau) {
-            s = atomicAdd(count, 1u);
-            if (s < cap) slot_node[s] = (u32)i;
-            else s = 0xFFFFFFFFu;
+        const long long d = indeg[i];
+        if (d >= tau_lo && d < tau_hi) {
+            const u32 k = atomicAdd(count, 1u);
+            if (k < cap) {
+                slot_node[base + k] = (u32)i;
+                node_slot[i] = base + k;
+            }
         }
-        node_slot[i] = s;
     }
 }
 
@@ -673,16 +746,17 @@ using namespace fr;
 struct fr_solver {
     long long n, m;
     int fp32;
-    int sel_grid, sweep_grid, thread_grid, warp_grid, block_grid;
-    u32 nhot;
+    int sel_grid, sweep_grid, thread_grid, warp_grid, block_grid, fold_grid;
+    u32 nhot, nslots;
     SolveCtl *ctl;
     fr_trace_row *trace;
     long long trace_cap;
     void *qnode_buf, *qval_buf;
     double *parts;
     u64 *parts64;
-    u32 *tgt_enc;      // fused path: column indices with hot targets encoded
+    u32 *tgt_enc;      // fused path: column indices with slotted targets encoded
     u32 *slot_node;
+    void *fw_buf;
     fr_solver_config cfg;
     cudaGraph_t graph;
     cudaGraphExec_t exec;
@@ -730,10 +804,11 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     if (a.path == PATH_FUSED) {
         // sweep -> hub pushes -> finalize -> (guarded) exact mass -> (guarded) check
-        cudaGraphNode_t n_sw, n_hub, n_fin, n_m, n_chk;
+        cudaGraphNode_t n_sw, n_hub, n_fold, n_fin, n_m, n_chk;
         FR_TRY(add_kernel<FT>(body, &n_sw, nullptr, 0, (void *)k_sweep<FT>, s->sweep_grid, SW_NT, args_a));
         FR_TRY(add_kernel<FT>(body, &n_hub, &n_sw, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
-        FR_TRY(add_kernel<FT>(body, &n_fin, &n_hub, 1, (void *)k_finalize<FT>, 1, FIN_NT, args_ans));
+        FR_TRY(add_kernel<FT>(body, &n_fold, &n_hub, 1, (void *)k_fold<FT>, s->fold_grid, 256, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_fin, &n_fold, 1, (void *)k_finalize<FT>, 1, FIN_NT, args_ans));
         FR_TRY(add_kernel<FT>(body, &n_m, &n_fin, 1, (void *)k_mass_partials<FT>, s->sel_grid, SEL_NT, args_m1));
         FR_TRY(add_kernel<FT>(body, &n_chk, &n_m, 1, (void *)k_mass_check<FT>, 1, FIN_NT, args_an));
     } else {
@@ -755,12 +830,17 @@ static int occupancy_grid(void *func, int threads, int sms) {
     return per * sms;
 }
 
-// Selects up to `want` highest in-degree nodes (those with in-degree >= the
-// smallest threshold tau whose count fits) and writes the solver-private
-// encoded column indices.  Skipped when no node is hot enough to matter.
+// Slot classes by in-degree: "hot" = up to `want_hot` highest in-degree nodes
+// (pushes summed in shared memory), "warm" = the next up to `want_warm` (pushes
+// into the compact array Fw).  A class is the largest threshold set that fits:
+// {indeg >= tau} with the smallest tau whose count does not exceed the budget.
+// Writes the solver-private encoded column indices.
 template <typename FT>
-static int prepare_hot(fr_solver *s, SweepArgs<FT> &a, int want) {
-    if (want > HOT_SLOTS) want = HOT_SLOTS;
+static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long want_warm) {
+    if (want_hot > HOT_SLOTS) want_hot = HOT_SLOTS;
+    if (want_hot < 0) want_hot = 0;
+    if (want_warm < 0) want_warm = 0;
+    if (want_warm > (long long)WARM_SLOTS * 8) want_warm = (long long)WARM_SLOTS * 8;
     const long long n = s->n, m = s->m;
     DeviceInfo di;
     FR_TRY(device_info(&di));
@@ -777,10 +857,6 @@ static int prepare_hot(fr_solver *s, SweepArgs<FT> &a, int want) {
     k_max_ll<<<g, 256, 0, st>>>(indeg, n, cnt);
     FR_CUDA(cudaMemcpyAsync(&hmax, cnt, sizeof(hmax), cudaMemcpyDeviceToHost, st));
     FR_CUDA(cudaStreamSynchronize(st));
-    const long long min_hot = 64;  // below this a target cannot serialise a sweep
-    if ((long long)hmax < min_hot) return FR_OK;
-    // smallest tau >= min_hot with count(indeg >= tau) <= want
-    long long lo = min_hot, hi = (long long)hmax;  // count(>= hi) >= 1
     auto count_ge = [&](long long tau, unsigned long long *out) -> int {
         FR_CUDA(cudaMemsetAsync(cnt, 0, sizeof(*cnt), st));
         k_count_ge<<<g, 256, 0, st>>>(indeg, n, tau, cnt);
@@ -788,37 +864,60 @@ static int prepare_hot(fr_solver *s, SweepArgs<FT> &a, int want) {
         FR_CUDA(cudaStreamSynchronize(st));
         return FR_OK;
     };
-    unsigned long long c_lo = 0;
-    FR_TRY(count_ge(lo, &c_lo));
-    long long tau = lo;
-    if (c_lo > (unsigned long long)want) {
-        while (hi - lo > 1) {  // invariant: count(lo) > want
+    // smallest tau >= floor with count(indeg >= tau) <= budget; hmax + 1 if none
+    auto threshold = [&](long long floor, unsigned long long budget, long long *tau_out) -> int {
+        if ((long long)hmax < floor || budget == 0) { *tau_out = (long long)hmax + 1; return FR_OK; }
+        unsigned long long c;
+        FR_TRY(count_ge(floor, &c));
+        if (c <= budget) { *tau_out = floor; return FR_OK; }
+        long long lo = floor, hi = (long long)hmax + 1;  // count(lo) > budget >= count(hi)
+        while (hi - lo > 1) {
             const long long mid = lo + (hi - lo) / 2;
-            unsigned long long c;
             FR_TRY(count_ge(mid, &c));
-            if (c > (unsigned long long)want) lo = mid; else hi = mid;
+            if (c > budget) lo = mid; else hi = mid;
         }
-        tau = hi;
-    }
+        *tau_out = hi;
+        return FR_OK;
+    };
+    // a target needs many pushes per sweep before an L2 slot or shared memory pays
+    long long tau_hot, tau_warm;
+    FR_TRY(threshold(64, (unsigned long long)want_hot, &tau_hot));
+    FR_TRY(threshold(8, (unsigned long long)(want_hot + want_warm), &tau_warm));
+    if (tau_warm > tau_hot) tau_warm = tau_hot;
     u32 *node_slot, *d_count;
     FR_TRY(scratch.alloc(&node_slot, (size_t)n));
     FR_TRY(scratch.alloc(&d_count, 1));
-    FR_CUDA(cudaMalloc(&s->slot_node, sizeof(u32) * HOT_SLOTS));
+    FR_CUDA(cudaMemsetAsync(node_slot, 0xFF, sizeof(u32) * (size_t)n, st));
+    const size_t cap = (size_t)want_hot + (size_t)want_warm;
+    if (cap == 0) return FR_OK;
+    FR_CUDA(cudaMalloc(&s->slot_node, sizeof(u32) * cap));
+    u32 nhot = 0, nwarm = 0;
     FR_CUDA(cudaMemsetAsync(d_count, 0, sizeof(u32), st));
-    k_collect_hot<<<g, 256, 0, st>>>(indeg, n, tau, (u32)want, s->slot_node, node_slot, d_count);
-    u32 nhot = 0;
+    k_collect_class<<<g, 256, 0, st>>>(indeg, n, tau_hot, LLONG_MAX, 0, (u32)want_hot, s->slot_node, node_slot, d_count);
     FR_CUDA(cudaMemcpyAsync(&nhot, d_count, sizeof(u32), cudaMemcpyDeviceToHost, st));
     FR_CUDA(cudaStreamSynchronize(st));
-    if (nhot > (u32)want) nhot = (u32)want;
-    if (nhot == 0) return FR_OK;
+    if (nhot > (u32)want_hot) nhot = (u32)want_hot;
+    FR_CUDA(cudaMemsetAsync(d_count, 0, sizeof(u32), st));
+    k_collect_class<<<g, 256, 0, st>>>(indeg, n, tau_warm, tau_hot, nhot, (u32)want_warm, s->slot_node, node_slot,
+                                       d_count);
+    FR_CUDA(cudaMemcpyAsync(&nwarm, d_count, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    FR_CUDA(cudaStreamSynchronize(st));
+    if (nwarm > (u32)want_warm) nwarm = (u32)want_warm;
+    const u32 nslots = nhot + nwarm;
+    if (nslots == 0) return FR_OK;
     FR_CUDA(cudaMalloc(&s->tgt_enc, sizeof(u32) * (size_t)m));
+    FR_CUDA(cudaMalloc(&s->fw_buf, sizeof(FT) * (size_t)nslots));
+    FR_CUDA(cudaMemsetAsync(s->fw_buf, 0, sizeof(FT) * (size_t)nslots, st));
     k_encode_targets<<<g, 256, 0, st>>>(a.tgt, m, node_slot, s->tgt_enc);
     FR_CUDA(cudaGetLastError());
     FR_CUDA(cudaStreamSynchronize(st));
     a.tgt = s->tgt_enc;
     a.slot_node = s->slot_node;
+    a.Fw = reinterpret_cast<FT *>(s->fw_buf);
     a.nhot = nhot;
+    a.nslots = nslots;
     s->nhot = nhot;
+    s->nslots = nslots;
     return FR_OK;
 }
 
@@ -884,8 +983,15 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.part_steps = s->parts64;
     a.part_sel = s->parts64 + P;
     a.slot_node = nullptr;
+    a.Fw = nullptr;
     a.nhot = 0;
-    if (a.path == PATH_FUSED && c.hot_slots >= 0 && m > 0) FR_TRY(prepare_hot(s, a, c.hot_slots ? c.hot_slots : HOT_SLOTS));
+    a.nslots = 0;
+    if (a.path == PATH_FUSED && m > 0) {
+        const int want_hot = c.hot_slots < 0 ? 0 : (c.hot_slots ? c.hot_slots : HOT_SLOTS);
+        const long long want_warm = c.warm_slots < 0 ? 0 : (c.warm_slots ? c.warm_slots : (long long)WARM_SLOTS);
+        FR_TRY(prepare_slots(s, a, want_hot, want_warm));
+    }
+    s->fold_grid = (int)std::max<long long>(1, std::min<long long>((long long)di.sms * 8, ((long long)a.nslots + 255) / 256));
     return build_graph<FT>(s, a);
 }
 
@@ -1015,6 +1121,7 @@ static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve
         FR_CUDA(cudaEventRecord(ev[3], st));
         k_push_block<FT><<<s->block_grid, BLK_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[4], st));
+        if (fused) k_fold<FT><<<s->fold_grid, 256, 0, st>>>(a);
         k_finalize<FT><<<1, FIN_NT, 0, st>>>(a, fused ? nparts_sw : nparts);
         if (fused) {
             k_mass_partials<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a, 1);
@@ -1077,6 +1184,7 @@ extern "C" int fr_solver_destroy(fr_solver *s) {
     cudaFree(s->parts64);
     cudaFree(s->tgt_enc);
     cudaFree(s->slot_node);
+    cudaFree(s->fw_buf);
     delete s;
     return FR_OK;
 }

@@ -32,7 +32,8 @@ class DeviceSchedule:
     """A selection rule plus its theta policy; consumed by engine.run."""
 
     def __init__(self, kind, seed=0, decay=0.5, policy="exhaust", rand_frac=0.25,
-                 mass_frac=0.5, thread_max_degree=0, block_min_degree=0, kernel_path="fused", hot_slots=0):
+                 mass_frac=0.5, thread_max_degree=0, block_min_degree=0, kernel_path="fused", hot_slots=0,
+                 warm_slots=0):
         if kind not in KINDS:
             raise ValueError(f"unknown scheduler kind {kind!r}; expected one of {KINDS}")
         if not 0.0 < decay < 1.0:
@@ -51,6 +52,7 @@ class DeviceSchedule:
             raise ValueError(f"kernel_path must be 'fused' or 'binned', got {kernel_path!r}")
         self.kernel_path = kernel_path
         self.hot_slots = int(hot_slots)
+        self.warm_slots = int(warm_slots)
         self._per_count = 0
         self._rng = None
 
@@ -82,6 +84,7 @@ class DeviceSchedule:
         c.seed = self.seed & 0xFFFFFFFF
         c.kernel_path = 0 if self.kernel_path == "fused" else 1
         c.hot_slots = self.hot_slots
+        c.warm_slots = self.warm_slots
         return c
 
     # -- reference single-node interface -------------------------------

@@ -225,14 +225,15 @@ def test_host_buffer_entry_point(cuda, golden_configs):
     assert l1(rank, golden_configs["cfg1_sweep_rank"]) <= L1_FP64
 
 
-@pytest.mark.parametrize("hot_slots", [-1, 0, 7])
-def test_hot_slot_aggregation(cuda, oracle, hot_slots):
+@pytest.mark.parametrize("hot_slots,warm_slots", [(-1, -1), (0, -1), (7, 0), (0, 0), (-1, 5000)])
+def test_hot_slot_aggregation(cuda, oracle, hot_slots, warm_slots):
     """Shared-memory aggregation of pushes into in-degree hubs keeps exact conservation."""
     src, dst = oracle.gen_edges(oracle.web_config(8.0), 200_000, 31)
     off, tgt, _ = oracle.csr_build(200_000, src, dst, clean=True)
     g = graph_from(cuda, off, tgt)
     params = cuda.DiffusionParams(target_error=1e-10)
-    sched = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9, hot_slots=hot_slots)
+    sched = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9, hot_slots=hot_slots,
+                                warm_slots=warm_slots)
     state = cuda.init(g, params)
     rank, trace = cuda.run(g, params, sched, state=state)
     ref = oracle.run_seq(off, tgt, 0.85, 1e-11, "sweep").rank

@@ -17,6 +17,26 @@ __device__ __forceinline__ void red_add(double *p, double v) {
 
 // mode 0: uniform random over [0, window) ; mode 1: i + (+-1000) local, i streamed in order
 // mode 2: like 1 but plain load + store (non-atomic, racy) to compare ; mode 3: atomicAdd (returning)
+// mode 11: local pattern, warps take 128-node chunks in order from a global counter
+__global__ void probe_dyn(double *F, long long n, long long total, unsigned long long *ctr) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned long long k = 0;
+        if (lane == 0) k = atomicAdd(ctr, 1ull);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        const long long base = (long long)k * 128;
+        if (base >= total) break;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const long long i = base + u * 32 + lane;
+            uint64_t h = mix((uint64_t)i * 0x9E37ull + 17);
+            long long off = (long long)(h % 2001) - 1000;
+            long long t = ((i % n) + off + n) % n;
+            red_add(F + t, 1.0);
+        }
+    }
+}
+
 __global__ void probe(double *F, long long n, long long window, long long per_thread, int mode, double *sink) {
     const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long nt = (long long)gridDim.x * blockDim.x;
@@ -85,6 +105,20 @@ int main() {
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         printf("%-36s %8.3f ms  %7.1f G ops/s\n", c.name, ms, per * nt / (ms * 1e6));
+    }
+    {
+        unsigned long long *ctr;
+        cudaMalloc(&ctr, 8);
+        for (int rep = 0; rep < 2; rep++) {
+            cudaMemset(ctr, 0, 8);
+            cudaEventRecord(a);
+            probe_dyn<<<blocks, threads>>>(F, n, per * nt, ctr);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            if (rep) printf("%-36s %8.3f ms  %7.1f G ops/s\n", "local, in-order dynamic chunks", ms, per * nt / (ms * 1e6));
+        }
     }
     cudaError_t e = cudaGetLastError();
     printf("status %s\n", cudaGetErrorString(e));
