@@ -163,6 +163,7 @@ typedef struct fr_solve_stats {
     double residual;          /* exact sum |F| after the run           */
     double theta;
     int64_t trace_len;
+    int64_t hub_edges;        /* edges pushed by the hub (block-per-node) kernel */
 } fr_solve_stats;
 
 typedef struct fr_solver fr_solver;

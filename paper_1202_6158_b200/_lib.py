@@ -55,7 +55,8 @@ class TraceRow(ctypes.Structure):
 class SolveStats(ctypes.Structure):
     _fields_ = [("diffusions", ctypes.c_int64), ("elementary_steps", ctypes.c_int64),
                 ("sweeps", ctypes.c_int64), ("residual", ctypes.c_double),
-                ("theta", ctypes.c_double), ("trace_len", ctypes.c_int64)]
+                ("theta", ctypes.c_double), ("trace_len", ctypes.c_int64),
+                ("hub_edges", ctypes.c_int64)]
 
 
 # every symbol the header declares, with its ctypes signature

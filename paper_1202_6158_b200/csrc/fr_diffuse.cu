@@ -48,6 +48,7 @@ struct SolveCtl {
     double last_max;    // max score seen by the last select pass
     double mass0;       // exact mass at the start of the solve
     u64 diffusions, steps, sweeps;
+    u64 hub_steps;      // edges pushed by the block-per-node hub kernel
     u64 trace_len;
     u32 qcount[3];
     u32 stop;
@@ -69,7 +70,7 @@ struct SweepArgs {
     u32 *qnode[3];
     FT *qval[3];
     double *part_mass, *part_abs, *part_max;
-    u64 *part_steps, *part_sel;
+    u64 *part_steps, *part_sel, *part_hsteps;
     const u32 *slot_node;  // slot -> node for the hot and warm classes (fused path)
     FT *Fw;                // compact fluid of the slotted nodes, folded into F every sweep
     u32 nhot;              // slots [0, nhot): shared-memory aggregated
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
     const u64 sweep = c->sweeps;
     const double keep_frac = 1.0 - a.d;
     double absorbed = 0.0, mx = 0.0;
-    u64 steps = 0, nsel = 0;
+    u64 steps = 0, nsel = 0, hsteps = 0;
     const long long ntiles = (a.n + 31) >> 5;
     const u32 *__restrict__ tgt = a.tgt;
     FT *__restrict__ F = a.F;
@@ -259,24 +260,30 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
     const long long seg_tiles = (ntiles + SW_SEGS - 1) / SW_SEGS;
     int seg = (int)((blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5)) % SW_SEGS), misses = 0;
     long long chunk_end = 0;
+    // the next chunk is reserved one chunk ahead, so the counter's atomic
+    // round trip overlaps the current chunk's work
+    unsigned long long pend = 0;
+    auto issue_grab = [&]() {
+        if (lane == 0) pend = atomicAdd(&a.ctl->seg_next[seg], (unsigned long long)SW_CHUNK);
+    };
     auto grab = [&](long long &t) -> bool {
-        while (misses < SW_SEGS) {
-            unsigned long long k = 0;
-            if (lane == 0) k = atomicAdd(&a.ctl->seg_next[seg], (unsigned long long)SW_CHUNK);
-            k = __shfl_sync(FULL, k, 0);
+        for (;;) {
+            const unsigned long long k = __shfl_sync(FULL, pend, 0);
             const long long s0 = (long long)seg * seg_tiles;
             const long long s1 = s0 + seg_tiles < ntiles ? s0 + seg_tiles : ntiles;
             if (s0 + (long long)k < s1) {
                 t = s0 + (long long)k;
                 chunk_end = t + SW_CHUNK < s1 ? t + SW_CHUNK : s1;
                 misses = 0;
+                issue_grab();
                 return true;
             }
             seg = (seg + 1) % SW_SEGS;
-            misses++;
+            if (++misses >= SW_SEGS) return false;
+            issue_grab();
         }
-        return false;
     };
+    issue_grab();
     long long tile = 0;
     bool have = grab(tile);
     // software pipeline: fluid and row offsets of the next tile are in flight
@@ -380,6 +387,7 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
                 const u32 q = hb + __popc(hmask & ((1u << lane) - 1u));
                 a.qnode[2][q] = (u32)i;
                 a.qval[2][q] = pvf;
+                hsteps += deg;
             }
         }
         // scatter, one batch of 32*SW_UNROLL edges in flight ahead of the reds
@@ -406,7 +414,9 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
     const double bx = block_max<SW_NT>(mx, red_sm);
     const u64 bs = block_sum_u64<SW_NT>(steps, red_sm64);
     const u64 bn = block_sum_u64<SW_NT>(nsel, red_sm64);
+    const u64 bh = block_sum_u64<SW_NT>(hsteps, red_sm64);
     if (threadIdx.x == 0) {
+        a.part_hsteps[blockIdx.x] = bh;
         a.part_abs[blockIdx.x] = ba;
         a.part_max[blockIdx.x] = bx;
         a.part_steps[blockIdx.x] = bs;
@@ -633,19 +643,21 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
     __shared__ double sm[FIN_NT / 32];
     __shared__ u64 sm64[FIN_NT / 32];
     double mass = 0.0, ab = 0.0, mx = 0.0;
-    u64 steps = 0, nsel = 0;
+    u64 steps = 0, nsel = 0, hsteps = 0;
     for (int p = threadIdx.x; p < nparts; p += FIN_NT) {
         mass += a.part_mass[p];
         ab += a.part_abs[p];
         mx = fmax(mx, a.part_max[p]);
         steps += a.part_steps[p];
         nsel += a.part_sel[p];
+        if (a.path == PATH_FUSED) hsteps += a.part_hsteps[p];
     }
     mass = block_sum<FIN_NT>(mass, sm);
     ab = block_sum<FIN_NT>(ab, sm);
     mx = block_max<FIN_NT>(mx, sm);
     steps = block_sum_u64<FIN_NT>(steps, sm64);
     nsel = block_sum_u64<FIN_NT>(nsel, sm64);
+    hsteps = block_sum_u64<FIN_NT>(hsteps, sm64);
     if (threadIdx.x != 0) return;
     SolveCtl *c = a.ctl;
     // binned path: the select pass saw F before any push of this sweep, so its
@@ -657,6 +669,7 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
     c->residual = residual;
     c->diffusions += nsel;
     c->steps += steps;
+    c->hub_steps += hsteps;
     c->sweeps += 1;
     c->last_max = mx;
     if (a.trace && c->trace_len < (u64)a.trace_cap) {
@@ -836,7 +849,7 @@ static int occupancy_grid(void *func, int threads, int sms) {
 // {indeg >= tau} with the smallest tau whose count does not exceed the budget.
 // Writes the solver-private encoded column indices.
 template <typename FT>
-static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long want_warm) {
+static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long want_warm, cudaStream_t st) {
     if (want_hot > HOT_SLOTS) want_hot = HOT_SLOTS;
     if (want_hot < 0) want_hot = 0;
     if (want_warm < 0) want_warm = 0;
@@ -844,7 +857,6 @@ static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long
     const long long n = s->n, m = s->m;
     DeviceInfo di;
     FR_TRY(device_info(&di));
-    cudaStream_t st = 0;
     Scratch scratch(st);
     long long *indeg;
     unsigned long long *cnt;
@@ -923,7 +935,7 @@ static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long
 
 template <typename FT>
 static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const uint32_t *d_targets,
-                 const double *d_w, void *d_fluid, double *d_history) {
+                 const double *d_w, void *d_fluid, double *d_history, cudaStream_t st) {
     DeviceInfo di;
     FR_TRY(device_info(&di));
     const fr_solver_config &c = s->cfg;
@@ -976,12 +988,13 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     if (s->sweep_grid > wtiles) s->sweep_grid = (int)std::max<long long>(1, wtiles);
     const int P = std::max(s->sel_grid, s->sweep_grid);
     FR_CUDA(cudaMalloc(&s->parts, sizeof(double) * 3 * (size_t)P));
-    FR_CUDA(cudaMalloc(&s->parts64, sizeof(u64) * 2 * (size_t)P));
+    FR_CUDA(cudaMalloc(&s->parts64, sizeof(u64) * 3 * (size_t)P));
     a.part_mass = s->parts;
     a.part_abs = s->parts + P;
     a.part_max = s->parts + 2 * P;
     a.part_steps = s->parts64;
     a.part_sel = s->parts64 + P;
+    a.part_hsteps = s->parts64 + 2 * P;
     a.slot_node = nullptr;
     a.Fw = nullptr;
     a.nhot = 0;
@@ -989,7 +1002,7 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     if (a.path == PATH_FUSED && m > 0) {
         const int want_hot = c.hot_slots < 0 ? 0 : (c.hot_slots ? c.hot_slots : HOT_SLOTS);
         const long long want_warm = c.warm_slots < 0 ? 0 : (c.warm_slots ? c.warm_slots : (long long)WARM_SLOTS);
-        FR_TRY(prepare_slots(s, a, want_hot, want_warm));
+        FR_TRY(prepare_slots(s, a, want_hot, want_warm, st));
     }
     s->fold_grid = (int)std::max<long long>(1, std::min<long long>((long long)di.sms * 8, ((long long)a.nslots + 255) / 256));
     return build_graph<FT>(s, a);
@@ -1021,7 +1034,6 @@ extern "C" int fr_solver_create(int64_t n, int64_t m, const int64_t *d_offsets, 
         set_error("fr_solver_create: op/op2 need per-node score weights");
         return FR_ERR_ARG;
     }
-    (void)stream;
     fr_solver *s = new fr_solver();
     s->n = n;
     s->m = m;
@@ -1036,8 +1048,11 @@ extern "C" int fr_solver_create(int64_t n, int64_t m, const int64_t *d_offsets, 
             rc = cuda_fail(cudaGetLastError(), "cudaMalloc(trace)", __FILE__, __LINE__);
             break;
         }
-        rc = s->fp32 ? setup<float>(s, s->af, d_offsets, d_targets, d_score_weight, d_fluid, d_history)
-                     : setup<double>(s, s->ad, d_offsets, d_targets, d_score_weight, d_fluid, d_history);
+        // all setup work is ordered on the caller's stream (its inputs may still be in flight there)
+        rc = s->fp32 ? setup<float>(s, s->af, d_offsets, d_targets, d_score_weight, d_fluid, d_history,
+                                    (cudaStream_t)stream)
+                     : setup<double>(s, s->ad, d_offsets, d_targets, d_score_weight, d_fluid, d_history,
+                                     (cudaStream_t)stream);
     } while (0);
     if (rc != FR_OK) {
         fr_solver_destroy(s);
@@ -1063,6 +1078,7 @@ static int read_stats(fr_solver *s, cudaStream_t st, fr_solve_stats *h) {
         h->residual = c.residual;
         h->theta = c.theta;
         h->trace_len = (int64_t)c.trace_len;
+        h->hub_edges = (int64_t)c.hub_steps;
     }
     return FR_OK;
 }

@@ -239,3 +239,22 @@ def test_hot_slot_aggregation(cuda, oracle, hot_slots, warm_slots):
     ref = oracle.run_seq(off, tgt, 0.85, 1e-11, "sweep").rank
     assert l1(rank, ref) <= 2e-10
     assert state.residual <= 1e-10 * 0.15
+
+
+def test_host_buffer_entry_point_with_hubs(cuda, oracle):
+    """fr_pagerank_host on a web graph whose in-degree hubs get shared-memory / warm slots:
+    the slot preparation must be ordered after the host-to-device copies."""
+    import ctypes
+    from paper_1202_6158_b200 import _lib
+    n = 300_000
+    src, dst = oracle.gen_edges(oracle.web_config(12.0), n, 17)
+    off, tgt, _ = oracle.csr_build(n, src, dst, clean=True)
+    cfg = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9).solver_config(
+        cuda.DiffusionParams(target_error=1e-10))
+    for _ in range(2):
+        rank = np.empty(n)
+        stats = _lib.SolveStats()
+        _lib.check(_lib.lib.fr_pagerank_host(n, tgt.size, off.ctypes.data, tgt.ctypes.data, ctypes.byref(cfg),
+                                             rank.ctypes.data, ctypes.byref(stats)))
+        ref = oracle.run_seq(off, tgt, 0.85, 1e-11, "sweep").rank
+        assert l1(rank, ref) <= 1e-9
