@@ -205,6 +205,26 @@ int fr_power_run(fr_power *p, double target_error, int64_t max_iterations, doubl
 int fr_power_destroy(fr_power *p);
 
 /* ------------------------------------------------------------------ */
+/* Batched personalized PageRank (BASELINE config 4): B <= 64 teleport */
+/* vectors diffuse together; fluid/history are n x B row-major fp64.   */
+/* Each column c is engine.py:240-341 run() with teleport V_c; column  */
+/* c stops once its residual <= target*(1-d) (checked exactly).        */
+/* ------------------------------------------------------------------ */
+typedef struct fr_ppr fr_ppr;
+/* F[s, c] += (1-d)/k for each of the k seeds s of column c (V_c uniform over
+ * its seeds, repeated seeds accumulate), H = 0.  d_seeds: B x k uint32. */
+int fr_ppr_init(int64_t n, int32_t B, const uint32_t *d_seeds, int32_t k, double damping, double *d_fluid,
+                double *d_history, void *stream);
+/* cfg: damping, target_error, decay (geometric theta), max_sweeps. */
+int fr_ppr_create(int64_t n, int64_t m, const int64_t *d_offsets, const uint32_t *d_targets, int32_t B,
+                  double *d_fluid, double *d_history, const fr_solver_config *cfg, void *stream, fr_ppr **out);
+/* h_col_residual (B): exact final residual of each column. */
+int fr_ppr_run(fr_ppr *p, void *stream, fr_solve_stats *h_stats, double *h_col_residual);
+int fr_ppr_destroy(fr_ppr *p);
+/* rank[:, c] = history[:, c] / sum |history[:, c]|. */
+int fr_ppr_normalize(int64_t n, int32_t B, const double *d_history, double *d_rank, void *stream);
+
+/* ------------------------------------------------------------------ */
 /* One call from host buffers (the reference-facing end-to-end path):  */
 /* H2D of the CSR, device solve, D2H of the normalized rank.           */
 /* engine.py:240-341 run(graph, params, scheduler) -> rank.            */

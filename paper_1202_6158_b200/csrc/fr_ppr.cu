@@ -1,0 +1,489 @@
+// fr_ppr.cu -- batched personalized PageRank by D-iteration (BASELINE config 4).
+//
+// B <= 64 personalization vectors V_c diffuse together: fluid F and history H
+// are n x B row-major fp64 arrays, so one visit of an edge scatters a B-wide
+// vector (each lane of a warp owns columns lane and lane + 32).  Every column
+// is an independent instance of engine.py:240-341 (teleport = V_c); the sweep
+// rule is the scalar solver's threshold sweep applied to the row maximum over
+// the columns that are still active, and column c stops (freezes: no more
+// pushes) once its residual R_c <= target*(1-d) is confirmed by an exact sum.
+#include <math.h>
+
+#include <algorithm>
+
+#include "fr_common.cuh"
+
+namespace fr {
+
+static constexpr int PP_NT = 256;
+static constexpr int PP_SEGS = 16;
+static constexpr int PP_CHUNK = 64;  // consecutive nodes per reservation (one warp per node)
+
+struct PprCtl {
+    double theta;
+    double resid[64];      // incremental residual per column
+    double exact[64];      // exact residual per column (after a check)
+    u64 active;            // bit c: column c still diffusing
+    u64 need_check;        // columns whose incremental residual crossed the target
+    u64 diffusions, steps, sweeps;
+    u64 seg_next[PP_SEGS];
+    u32 stop;
+    u32 pad;
+};
+
+struct PprArgs {
+    double *F, *H;
+    const u64 *off;
+    const u32 *tgt;
+    PprCtl *ctl;
+    double *part_abs;    // [grid][64]
+    double *part_max;    // [grid]
+    u64 *part_sel, *part_steps;
+    double *part_mass;   // [grid][64] for exact checks
+    long long n;
+    int B;
+    int nparts;
+    double d, thr, decay;
+    long long max_sweeps;
+    int in_graph;
+    cudaGraphConditionalHandle cond;
+};
+
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Warp per node, nodes taken in order from PP_SEGS segments (as the scalar sweep).
+__global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
+    __shared__ double s_abs[PP_NT / 32][64];
+    __shared__ double s_red[PP_NT / 32];
+    __shared__ u64 s_red64[PP_NT / 32];
+    constexpr u32 FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    PprCtl *c = a.ctl;
+    const double theta = c->theta;
+    const u64 active = c->active;
+    const int B = a.B;
+    const bool own0 = lane < B && ((active >> lane) & 1ull);
+    const bool own1 = lane + 32 < B && ((active >> (lane + 32)) & 1ull);
+    double ab0 = 0.0, ab1 = 0.0, mx = 0.0;
+    u64 nsel = 0, steps = 0;
+    const long long seg_len = (a.n + PP_SEGS - 1) / PP_SEGS;
+    int seg = (int)((blockIdx.x * (PP_NT / 32) + wid) % PP_SEGS), misses = 0;
+    long long node = 0, chunk_end = 0;
+    auto grab = [&]() -> bool {
+        while (misses < PP_SEGS) {
+            unsigned long long k = 0;
+            if (lane == 0) k = atomicAdd(&c->seg_next[seg], (unsigned long long)PP_CHUNK);
+            k = __shfl_sync(FULL, k, 0);
+            const long long s0 = (long long)seg * seg_len;
+            const long long s1 = s0 + seg_len < a.n ? s0 + seg_len : a.n;
+            if (s0 + (long long)k < s1) {
+                node = s0 + (long long)k;
+                chunk_end = node + PP_CHUNK < s1 ? node + PP_CHUNK : s1;
+                misses = 0;
+                return true;
+            }
+            seg = (seg + 1) % PP_SEGS;
+            misses++;
+        }
+        return false;
+    };
+    bool have = grab();
+    while (have) {
+        const long long i = node;
+        double *Fi = a.F + (size_t)i * B;
+        const double f0 = own0 ? Fi[lane] : 0.0;
+        const double f1 = own1 ? Fi[lane + 32] : 0.0;
+        const double rowmax = warp_max_d(fmax(fabs(f0), fabs(f1)));
+        mx = fmax(mx, rowmax);
+        if (rowmax >= theta && rowmax > 0.0) {
+            const u64 lo = a.off[i], hi = a.off[i + 1];
+            const u32 deg = (u32)(hi - lo);
+            double s0 = 0.0, s1 = 0.0;
+            if (own0) s0 = __longlong_as_double((long long)atomicExch((unsigned long long *)(Fi + lane), 0ull));
+            if (own1) s1 = __longlong_as_double((long long)atomicExch((unsigned long long *)(Fi + lane + 32), 0ull));
+            double *Hi = a.H + (size_t)i * B;
+            if (own0) Hi[lane] += s0;
+            if (own1) Hi[lane + 32] += s1;
+            nsel++;
+            if (deg == 0) {
+                ab0 += fabs(s0);
+                ab1 += fabs(s1);
+            } else {
+                ab0 += fabs(s0) * (1.0 - a.d);
+                ab1 += fabs(s1) * (1.0 - a.d);
+                steps += deg;
+                const double w = a.d / (double)deg;
+                const double p0 = s0 * w, p1 = s1 * w;  // sent*(d/deg), engine.py:321
+                for (u32 k0 = 0; k0 < deg; k0 += 32) {
+                    const u32 cnt = deg - k0 < 32u ? deg - k0 : 32u;
+                    const u32 tv = lane < cnt ? __ldg(a.tgt + lo + k0 + lane) : 0u;
+                    for (u32 j = 0; j < cnt; j++) {
+                        const u32 t = __shfl_sync(FULL, tv, j);
+                        double *Ft = a.F + (size_t)t * B;
+                        if (own0 && p0 != 0.0) red_add(Ft + lane, p0);
+                        if (own1 && p1 != 0.0) red_add(Ft + lane + 32, p1);
+                    }
+                }
+            }
+        }
+        node++;
+        have = node < chunk_end ? true : grab();
+    }
+    // per-column absorbed mass: lanes own columns, reduce over the block's warps
+    s_abs[wid][lane] = ab0;
+    s_abs[wid][lane + 32] = ab1;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        double t = 0.0;
+        for (int w = 0; w < PP_NT / 32; w++) t += s_abs[w][threadIdx.x];
+        a.part_abs[(size_t)blockIdx.x * 64 + threadIdx.x] = t;
+    }
+    const double bmx = block_max<PP_NT>(mx, s_red);
+    const u64 bsel = block_sum_u64<PP_NT>(nsel, s_red64);
+    const u64 bst = block_sum_u64<PP_NT>(steps, s_red64);
+    if (threadIdx.x == 0) {
+        a.part_max[blockIdx.x] = bmx;
+        a.part_sel[blockIdx.x] = bsel;
+        a.part_steps[blockIdx.x] = bst;
+    }
+}
+
+// Column masses |F_c|_1 (all columns, or only when a check is pending).
+__global__ void __launch_bounds__(PP_NT) k_ppr_mass(PprArgs a, int guarded) {
+    __shared__ double s[PP_NT / 32][64];
+    if (guarded && !a.ctl->need_check) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ double s_red[PP_NT / 32];
+    const int B = a.B;
+    double m0 = 0.0, m1 = 0.0, mx = 0.0;
+    for (long long i = blockIdx.x * (long long)(PP_NT / 32) + wid; i < a.n; i += (long long)gridDim.x * (PP_NT / 32)) {
+        const double *Fi = a.F + (size_t)i * B;
+        if (lane < B) m0 += fabs(Fi[lane]);
+        if (lane + 32 < B) m1 += fabs(Fi[lane + 32]);
+        if (lane < B) mx = fmax(mx, fabs(Fi[lane]));
+        if (lane + 32 < B) mx = fmax(mx, fabs(Fi[lane + 32]));
+    }
+    s[wid][lane] = m0;
+    s[wid][lane + 32] = m1;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        double t = 0.0;
+        for (int w = 0; w < PP_NT / 32; w++) t += s[w][threadIdx.x];
+        a.part_mass[(size_t)blockIdx.x * 64 + threadIdx.x] = t;
+    }
+    mx = block_max<PP_NT>(mx, s_red);
+    if (threadIdx.x == 0) a.part_max[blockIdx.x] = mx;
+}
+
+// Prologue (check = 0) and exact check (check = 1): one block of 64 threads.
+__global__ void k_ppr_settle(PprArgs a, int check) {
+    PprCtl *c = a.ctl;
+    const int col = threadIdx.x;
+    if (check && !c->need_check) return;
+    double t = 0.0;
+    for (int p = 0; p < a.nparts; p++) t += a.part_mass[(size_t)p * 64 + col];
+    __shared__ u64 s_done;
+    if (col == 0) s_done = 0;
+    __syncthreads();
+    if (col < a.B) {
+        const bool pending = !check || ((c->need_check >> col) & 1ull);
+        if (pending) {
+            c->exact[col] = t;
+            c->resid[col] = t;
+            if (t <= a.thr) atomicOr(&s_done, 1ull << col);
+        }
+    }
+    __syncthreads();
+    if (col == 0) {
+        if (!check) {  // prologue: the threshold starts at the largest fluid (sched.py:89-90)
+            double mx = 0.0;
+            for (int p = 0; p < a.nparts; p++) mx = fmax(mx, a.part_max[p]);
+            c->theta = mx;
+        }
+        c->active &= ~s_done;
+        c->need_check = 0;
+        const bool stop = c->active == 0 || (long long)c->sweeps >= a.max_sweeps;
+        c->stop = stop ? 1u : 0u;
+        if (a.in_graph) cudaGraphSetConditional(a.cond, stop ? 0u : 1u);
+    }
+}
+
+__global__ void k_ppr_finalize(PprArgs a) {
+    PprCtl *c = a.ctl;
+    const int col = threadIdx.x;  // 64 threads
+    double ab = 0.0;
+    for (int p = 0; p < a.nparts; p++) ab += a.part_abs[(size_t)p * 64 + col];
+    __shared__ u64 s_need;
+    __shared__ double s_max;
+    if (col == 0) {
+        s_need = 0;
+        double mx = 0.0;
+        u64 sel = 0, st = 0;
+        for (int p = 0; p < a.nparts; p++) {
+            mx = fmax(mx, a.part_max[p]);
+            sel += a.part_sel[p];
+            st += a.part_steps[p];
+        }
+        s_max = mx;
+        c->diffusions += sel;
+        c->steps += st;
+        c->sweeps += 1;
+        for (int q = 0; q < PP_SEGS; q++) c->seg_next[q] = 0;
+    }
+    __syncthreads();
+    if (col < a.B && ((c->active >> col) & 1ull)) {
+        const double r = c->resid[col] - ab;
+        c->resid[col] = r;
+        if (r <= a.thr) atomicOr(&s_need, 1ull << col);
+    }
+    __syncthreads();
+    if (col == 0) {
+        double th = c->theta * a.decay;
+        const double mx = s_max;
+        if (mx > 0.0)
+            while (th > mx) th *= a.decay;
+        c->theta = th;
+        // a column drained to zero everywhere also needs its exact check
+        c->need_check = s_need | (mx == 0.0 ? c->active : 0ull);
+        const bool stop = (long long)c->sweeps >= a.max_sweeps;
+        c->stop = stop ? 1u : 0u;
+        if (a.in_graph) cudaGraphSetConditional(a.cond, stop ? 0u : 1u);
+    }
+}
+
+__global__ void k_ppr_init(long long n, int B, int k, const u32 *__restrict__ seeds, double damping, double *F,
+                           double *H) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * (long long)B;
+         e += (long long)gridDim.x * blockDim.x) {
+        F[e] = 0.0;
+        H[e] = 0.0;
+    }
+}
+__global__ void k_ppr_seed(int B, int k, const u32 *__restrict__ seeds, double damping, double *F) {
+    // V_c uniform over the k seeds of column c: F = (1-d) * V_c (repeated seeds accumulate)
+    const int c = blockIdx.x;
+    for (int j = threadIdx.x; j < k; j += blockDim.x)
+        atomicAdd(F + (size_t)seeds[(size_t)c * k + j] * B + c, (1.0 - damping) * (1.0 / (double)k));
+}
+
+__global__ void k_ppr_colsum(long long n, int B, const double *__restrict__ H, double *out) {
+    __shared__ double s[PP_NT / 32][64];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double m0 = 0.0, m1 = 0.0;
+    for (long long i = blockIdx.x * (long long)(PP_NT / 32) + wid; i < n; i += (long long)gridDim.x * (PP_NT / 32)) {
+        if (lane < B) m0 += fabs(H[(size_t)i * B + lane]);
+        if (lane + 32 < B) m1 += fabs(H[(size_t)i * B + lane + 32]);
+    }
+    s[wid][lane] = m0;
+    s[wid][lane + 32] = m1;
+    __syncthreads();
+    if (threadIdx.x < 64 && threadIdx.x < B) {
+        double t = 0.0;
+        for (int w = 0; w < PP_NT / 32; w++) t += s[w][threadIdx.x];
+        atomicAdd(out + threadIdx.x, t);
+    }
+}
+__global__ void k_ppr_scale(long long n, int B, const double *__restrict__ H, const double *__restrict__ tot,
+                            double *R) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * (long long)B;
+         e += (long long)gridDim.x * blockDim.x) {
+        const double t = tot[e % B];
+        R[e] = t > 0.0 ? H[e] / t : H[e];
+    }
+}
+
+}  // namespace fr
+
+using namespace fr;
+
+struct fr_ppr {
+    long long n, m;
+    int B, grid;
+    PprArgs a;
+    PprCtl *ctl;
+    double *parts;
+    u64 *parts64;
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    fr_solver_config cfg;
+};
+
+static int ppr_add(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *dep, void *func, int grid, int block,
+                   void **args) {
+    cudaKernelNodeParams p = {};
+    p.func = func;
+    p.gridDim = dim3((unsigned)grid);
+    p.blockDim = dim3((unsigned)block);
+    p.kernelParams = args;
+    FR_CUDA(cudaGraphAddKernelNode(node, g, dep, dep ? 1 : 0, &p));
+    return FR_OK;
+}
+
+extern "C" int fr_ppr_destroy(fr_ppr *p) {
+    if (!p) return FR_OK;
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    cudaFree(p->ctl);
+    cudaFree(p->parts);
+    cudaFree(p->parts64);
+    delete p;
+    return FR_OK;
+}
+
+extern "C" int fr_ppr_init(int64_t n, int32_t B, const uint32_t *d_seeds, int32_t k, double damping, double *d_fluid,
+                           double *d_history, void *stream) {
+    if (n < 1 || B < 1 || B > 64 || k < 1 || !d_seeds || !d_fluid || !d_history) {
+        set_error("fr_ppr_init: need n >= 1, 1 <= B <= 64, k >= 1 and buffers");
+        return FR_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    DeviceInfo di;
+    FR_TRY(device_info(&di));
+    k_ppr_init<<<di.sms * 8, 256, 0, st>>>(n, B, k, d_seeds, damping, d_fluid, d_history);
+    k_ppr_seed<<<B, 128, 0, st>>>(B, k, d_seeds, damping, d_fluid);
+    FR_CUDA(cudaGetLastError());
+    return FR_OK;
+}
+
+extern "C" int fr_ppr_create(int64_t n, int64_t m, const int64_t *d_offsets, const uint32_t *d_targets, int32_t B,
+                             double *d_fluid, double *d_history, const fr_solver_config *cfg, void *stream,
+                             fr_ppr **out) {
+    if (!out || !cfg || n < 1 || n > 0xFFFFFFFFll || m < 0 || B < 1 || B > 64 || !d_offsets || !d_fluid ||
+        !d_history || (m > 0 && !d_targets)) {
+        set_error("fr_ppr_create: bad arguments (1 <= B <= 64)");
+        return FR_ERR_ARG;
+    }
+    if (!(cfg->damping > 0.0 && cfg->damping < 1.0) || !(cfg->target_error > 0.0) ||
+        !(cfg->decay > 0.0 && cfg->decay < 1.0)) {
+        set_error("fr_ppr_create: need 0 < damping < 1, target_error > 0, 0 < decay < 1");
+        return FR_ERR_ARG;
+    }
+    (void)stream;
+    DeviceInfo di;
+    FR_TRY(device_info(&di));
+    fr_ppr *p = new fr_ppr();
+    p->n = n;
+    p->m = m;
+    p->B = B;
+    p->cfg = *cfg;
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ppr_sweep, PP_NT, 0);
+    p->grid = std::max(1, per) * di.sms;
+    int rc = FR_OK;
+    do {
+        cudaError_t e;
+        if ((e = cudaMalloc(&p->ctl, sizeof(PprCtl))) != cudaSuccess ||
+            (e = cudaMalloc(&p->parts, sizeof(double) * (size_t)p->grid * (64 + 1 + 64))) != cudaSuccess ||
+            (e = cudaMalloc(&p->parts64, sizeof(u64) * (size_t)p->grid * 2)) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaMalloc(ppr)", __FILE__, __LINE__);
+            break;
+        }
+        PprArgs &a = p->a;
+        a.F = d_fluid;
+        a.H = d_history;
+        a.off = reinterpret_cast<const u64 *>(d_offsets);
+        a.tgt = d_targets;
+        a.ctl = p->ctl;
+        a.part_abs = p->parts;
+        a.part_max = p->parts + (size_t)p->grid * 64;
+        a.part_mass = p->parts + (size_t)p->grid * 65;
+        a.part_sel = p->parts64;
+        a.part_steps = p->parts64 + p->grid;
+        a.n = n;
+        a.B = B;
+        a.nparts = p->grid;
+        a.d = cfg->damping;
+        a.thr = cfg->target_error * (1.0 - cfg->damping);
+        a.decay = cfg->decay;
+        a.max_sweeps = cfg->max_sweeps > 0 ? cfg->max_sweeps : 1000000;
+        // graph: prologue (theta0, masses, settle) then while { sweep, finalize, mass?, check? }
+        if ((e = cudaGraphCreate(&p->graph, 0)) != cudaSuccess ||
+            (e = cudaGraphConditionalHandleCreate(&a.cond, p->graph, 0, 0)) != cudaSuccess) {
+            rc = cuda_fail(e, "graph", __FILE__, __LINE__);
+            break;
+        }
+        a.in_graph = 1;
+        static int zero = 0, one = 1;
+        void *args[] = {&a};
+        void *args0[] = {&a, &zero};
+        void *args1[] = {&a, &one};
+        cudaGraphNode_t n1, n2, nw;
+        if ((rc = ppr_add(p->graph, &n1, nullptr, (void *)k_ppr_mass, p->grid, PP_NT, args0)) != FR_OK) break;
+        if ((rc = ppr_add(p->graph, &n2, &n1, (void *)k_ppr_settle, 1, 64, args0)) != FR_OK) break;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = a.cond;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        if ((e = cudaGraphAddNode(&nw, p->graph, &n2, 1, &cp)) != cudaSuccess) {
+            rc = cuda_fail(e, "while node", __FILE__, __LINE__);
+            break;
+        }
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaGraphNode_t b0, b1, b2, b3;
+        if ((rc = ppr_add(body, &b0, nullptr, (void *)k_ppr_sweep, p->grid, PP_NT, args)) != FR_OK) break;
+        if ((rc = ppr_add(body, &b1, &b0, (void *)k_ppr_finalize, 1, 64, args)) != FR_OK) break;
+        if ((rc = ppr_add(body, &b2, &b1, (void *)k_ppr_mass, p->grid, PP_NT, args1)) != FR_OK) break;
+        if ((rc = ppr_add(body, &b3, &b2, (void *)k_ppr_settle, 1, 64, args1)) != FR_OK) break;
+        if ((e = cudaGraphInstantiate(&p->exec, p->graph, 0)) != cudaSuccess) {
+            rc = cuda_fail(e, "instantiate", __FILE__, __LINE__);
+            break;
+        }
+    } while (0);
+    if (rc != FR_OK) {
+        fr_ppr_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return FR_OK;
+}
+
+extern "C" int fr_ppr_run(fr_ppr *p, void *stream, fr_solve_stats *h_stats, double *h_col_residual) {
+    if (!p) { set_error("fr_ppr_run: null handle"); return FR_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    PprCtl init = {};
+    init.active = p->B == 64 ? ~0ull : ((1ull << p->B) - 1ull);
+    FR_CUDA(cudaMemcpyAsync(p->ctl, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+    FR_CUDA(cudaGraphLaunch(p->exec, st));
+    PprCtl c;
+    FR_CUDA(cudaMemcpyAsync(&c, p->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+    FR_CUDA(cudaStreamSynchronize(st));
+    if (h_stats) {
+        h_stats->diffusions = (int64_t)c.diffusions;
+        h_stats->elementary_steps = (int64_t)c.steps;
+        h_stats->sweeps = (int64_t)c.sweeps;
+        double mx = 0.0;
+        for (int col = 0; col < p->B; col++) mx = std::max(mx, c.exact[col]);
+        h_stats->residual = mx;
+        h_stats->theta = c.theta;
+        h_stats->trace_len = 0;
+        h_stats->hub_edges = 0;
+    }
+    if (h_col_residual)
+        for (int col = 0; col < p->B; col++) h_col_residual[col] = c.exact[col];
+    if (c.active) {
+        set_error("batched PPR: %d columns did not converge within the sweep budget", __builtin_popcountll(c.active));
+        return FR_ERR_NO_CONVERGENCE;
+    }
+    return FR_OK;
+}
+
+extern "C" int fr_ppr_normalize(int64_t n, int32_t B, const double *d_history, double *d_rank, void *stream) {
+    if (n < 1 || B < 1 || B > 64 || !d_history || !d_rank) { set_error("fr_ppr_normalize: bad arguments"); return FR_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    DeviceInfo di;
+    FR_TRY(device_info(&di));
+    Scratch scratch(st);
+    double *tot;
+    FR_TRY(scratch.alloc(&tot, 64));
+    FR_CUDA(cudaMemsetAsync(tot, 0, sizeof(double) * 64, st));
+    k_ppr_colsum<<<di.sms * 4, PP_NT, 0, st>>>(n, B, d_history, tot);
+    k_ppr_scale<<<di.sms * 8, 256, 0, st>>>(n, B, d_history, tot, d_rank);
+    FR_CUDA(cudaGetLastError());
+    FR_CUDA(cudaStreamSynchronize(st));
+    return FR_OK;
+}
