@@ -1,0 +1,47 @@
+"""BASELINE configs at full size.
+
+config 2 (N=1M) is small enough for the CPU oracle: bit-exact generator/CSR and
+rank parity.  config 3 (N=20M) is checked through size-independent
+properties: the fp64 D-iteration agrees with the independent power-iteration
+solver, the fp32-fluid variant stays within its stated tolerance of fp64, and
+the stopping rule and conservation hold.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def test_config2_full_size_parity(cuda, oracle):
+    from paper_1202_6158_b200 import gen
+    n, seed = 1_000_000, 2
+    g, rep = gen.generate(gen.web_config(8.0), n, seed)
+    src, dst = oracle.gen_edges(oracle.web_config(8.0), n, seed)
+    off, tgt, stats = oracle.csr_build(n, src, dst, clean=True)
+    assert np.array_equal(g.out_offsets.cpu().numpy(), off)
+    assert np.array_equal(g.out_targets.cpu().numpy().astype(np.uint32), tgt)
+    assert (rep.realized_links, rep.duplicates, rep.self_loops) == stats
+    params = cuda.DiffusionParams(target_error=1e-10)
+    sched = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9)
+    rank, trace = cuda.run(g, params, sched)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-12, "sweep")
+    assert float(np.abs(rank.cpu().numpy() - ref.rank).sum()) <= 1e-9
+    assert trace.rows[-1].residual <= 1e-10 * 0.15
+
+
+def test_config3_fp32_tolerance_and_power_iteration(cuda):
+    from paper_1202_6158_b200 import gen
+    g, rep = gen.generate(gen.web_config(10.0), 20_000_000, 3)
+    params = cuda.DiffusionParams(target_error=1e-9)
+    sched = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9)
+    state = cuda.init(g, params)
+    r64, _ = cuda.run(g, params, sched, state=state)
+    assert state.residual <= 1e-9 * 0.15
+    assert abs(float(r64.sum()) - 1.0) < 1e-12
+    r32, _ = cuda.run(g, params, sched, fluid_dtype=torch.float32)
+    # stated tolerance of the fp32-fluid / fp64-history variant
+    assert float((r32 - r64).abs().sum()) <= 1e-6
+    x, trace = cuda.power_iterate(g, cuda.DiffusionParams(target_error=1e-10))
+    assert float((x - r64).abs().sum()) <= 5e-9
