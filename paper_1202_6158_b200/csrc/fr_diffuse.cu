@@ -41,6 +41,8 @@ static constexpr int FIN_NT = 256;
 static constexpr int BLK_NT = 512;
 static constexpr int BLK_CHUNK = 2048;  // uint32 column indices per stage (8 KB)
 static constexpr int BLK_STAGES = 3;
+static constexpr int SW_MAX_SEGS = 256;
+static constexpr int SEG_PAD = 16;  // u64 per counter: one 128-byte line per segment counter
 
 struct SolveCtl {
     double theta;       // threshold of the next sweep
@@ -54,7 +56,7 @@ struct SolveCtl {
     u32 stop;
     u32 need_check;     // fused path: incremental residual crossed the target, verify exactly
     u32 pad;
-    u64 seg_next[16];   // fused path: in-order tile counters, one per node segment
+    u64 seg_next[SW_MAX_SEGS * SEG_PAD];  // fused path: in-order tile counters, one 128 B line each
 };
 
 enum { PATH_FUSED = 0, PATH_BINNED = 1 };
@@ -85,6 +87,8 @@ struct SweepArgs {
     int select, policy;
     u32 seed;
     int path;
+    int segs;    // fused path: in-order segments (<= SW_MAX_SEGS)
+    u32 chunk;   // fused path: tiles per reservation
     int in_graph;
     cudaGraphConditionalHandle cond;
 };
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(FIN_NT) k_prologue(SweepArgs<FT> a, int nparts
         c->residual = mass;
         c->mass0 = mass;
         c->qcount[0] = c->qcount[1] = c->qcount[2] = 0;
-        for (int q = 0; q < 16; q++) c->seg_next[q] = 0;
+        for (int q = 0; q < SW_MAX_SEGS; q++) c->seg_next[q * SEG_PAD] = 0;
         c->stop = (mass <= a.thr || mass == 0.0) ? 1u : 0u;
         if (a.in_graph) cudaGraphSetConditional(a.cond, c->stop ? 0u : 1u);
     }
@@ -210,8 +214,7 @@ __global__ void __launch_bounds__(256) k_fold(SweepArgs<FT> a) {
 // ------------------------------------------------------------------ fused sweep (default path)
 static constexpr int SW_NT = 256;
 static constexpr int SW_UNROLL = 4;
-static constexpr int SW_SEGS = 16;
-static constexpr int SW_CHUNK = 8;
+
 
 __device__ __forceinline__ double take_fluid(double *p) {
     return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
@@ -257,6 +260,8 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
     // that neighbouring sources push into (local targets) are hit while they
     // are still in L2 instead of being refilled (tools/red_probe.cu: in-order
     // chunks reach the minimum DRAM traffic, free-running warps ~1.8x it).
+    const int SW_SEGS = a.segs;
+    const u32 SW_CHUNK = a.chunk;
     const long long seg_tiles = (ntiles + SW_SEGS - 1) / SW_SEGS;
     int seg = (int)((blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5)) % SW_SEGS), misses = 0;
     long long chunk_end = 0;
@@ -264,7 +269,7 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
     // round trip overlaps the current chunk's work
     unsigned long long pend = 0;
     auto issue_grab = [&]() {
-        if (lane == 0) pend = atomicAdd(&a.ctl->seg_next[seg], (unsigned long long)SW_CHUNK);
+        if (lane == 0) pend = atomicAdd(&a.ctl->seg_next[seg * SEG_PAD], (unsigned long long)SW_CHUNK);
     };
     auto grab = [&](long long &t) -> bool {
         for (;;) {
@@ -694,7 +699,7 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
         while (th > mx) th *= a.decay;
     c->theta = th;
     c->qcount[0] = c->qcount[1] = c->qcount[2] = 0;
-    for (int q = 0; q < 16; q++) c->seg_next[q] = 0;
+    for (int q = 0; q < SW_MAX_SEGS; q++) c->seg_next[q * SEG_PAD] = 0;
     const bool budget = (long long)c->sweeps >= a.max_sweeps ||
                         (a.max_diffusions > 0 && (long long)c->diffusions >= a.max_diffusions);
     bool done;
@@ -962,6 +967,15 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.policy = c.policy;
     a.seed = c.seed;
     a.path = c.kernel_path == 1 ? PATH_BINNED : PATH_FUSED;
+    {
+        // tuning knobs for experiments (tools/prof_solver.py); defaults measured on config 5
+        const char *e1 = getenv("FR_SEGS"), *e2 = getenv("FR_CHUNK");
+        a.segs = e1 ? atoi(e1) : 64;
+        a.chunk = e2 ? (u32)atoi(e2) : 8u;
+        if (a.segs < 1) a.segs = 1;
+        if (a.segs > SW_MAX_SEGS) a.segs = SW_MAX_SEGS;
+        if (a.chunk < 1) a.chunk = 1;
+    }
     // queues: a selected node lands in exactly one bin
     const long long n = s->n, m = s->m;
     const long long cap0 = n;
