@@ -154,6 +154,7 @@ typedef struct fr_trace_row {
     int64_t sweeps;
     double residual;          /* fluid mass left (R of ALGO-REF)       */
     double theta;             /* threshold used by this sweep          */
+    int64_t t_ns;             /* device clock (%globaltimer) at the end of the sweep */
 } fr_trace_row;
 
 typedef struct fr_solve_stats {

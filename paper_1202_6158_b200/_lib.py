@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfluidrank_b200.so")
+# FR_LIB_PATH: development override to load a variant build (tools/build_variant.sh)
+LIB_PATH = os.environ.get("FR_LIB_PATH") or os.path.join(_HERE, "libfluidrank_b200.so")
 
 FR_OK = 0
 FR_ERR_RANGE = 1
@@ -49,7 +50,7 @@ class SolverConfig(ctypes.Structure):
 class TraceRow(ctypes.Structure):
     _fields_ = [("elementary_steps", ctypes.c_int64), ("diffusions", ctypes.c_int64),
                 ("sweeps", ctypes.c_int64), ("residual", ctypes.c_double),
-                ("theta", ctypes.c_double)]
+                ("theta", ctypes.c_double), ("t_ns", ctypes.c_int64)]
 
 
 class SolveStats(ctypes.Structure):

@@ -26,6 +26,7 @@
 #include <stdlib.h>
 
 #include <climits>
+#include <cstddef>
 
 #include <algorithm>
 #include <vector>
@@ -56,6 +57,8 @@ struct SolveCtl {
     u32 stop;
     u32 need_check;     // fused path: incremental residual crossed the target, verify exactly
     u32 pad;
+    double exact;       // sum |F| after the run (fr_solver_run)
+    // everything above is the header copied back after a run
     u64 seg_next[SW_MAX_SEGS * SEG_PAD];  // fused path: in-order tile counters, one 128 B line each
 };
 
@@ -212,8 +215,18 @@ __global__ void __launch_bounds__(256) k_fold(SweepArgs<FT> a) {
 }
 
 // ------------------------------------------------------------------ fused sweep (default path)
-static constexpr int SW_NT = 256;
-static constexpr int SW_UNROLL = 4;
+#ifndef FR_SW_NT
+#define FR_SW_NT 256
+#endif
+#ifndef FR_SW_UNROLL
+#define FR_SW_UNROLL 2
+#endif
+#ifndef FR_SW_PF
+#define FR_SW_PF 3
+#endif
+static constexpr int SW_NT = FR_SW_NT;
+static constexpr int SW_PF = FR_SW_PF;  // L2 prefetch distance in tiles
+static constexpr int SW_UNROLL = FR_SW_UNROLL;
 
 
 __device__ __forceinline__ double take_fluid(double *p) {
@@ -236,7 +249,10 @@ __device__ __forceinline__ u32 warp_sum_u32(u32 v) { return __reduce_add_sync(0x
 //     red.global.add of sent*d/deg into F;
 //   * hub rows (deg >= t2) are queued for the block-per-node kernel.
 template <typename FT>
-__global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
+#ifndef FR_SW_MINB
+#define FR_SW_MINB 4
+#endif
+__global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
     __shared__ double red_sm[SW_NT / 32];
     __shared__ u64 red_sm64[SW_NT / 32];
     __shared__ FT hot_acc[HOT_SLOTS];
@@ -309,6 +325,18 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
         FT f_nx = (FT)0;
         u64 lo_nx = 0, end_nx = 0;
         if (have_nx) load_tile(nxt, f_nx, lo_nx, end_nx);
+        {
+            // warm L2 with the fluid and offsets of a tile further ahead in the chunk
+            // (no registers held), so the register prefetch above hits L2
+            const long long pf = tile + SW_PF;
+            if (pf < chunk_end && (lane & 15) == 0) {
+                const long long j = (pf << 5) + lane;
+                if (j < a.n) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(F + j));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.off + j));
+                }
+            }
+        }
 
         const long long i = (tile << 5) + lane;
         const bool valid = i < a.n;
@@ -346,9 +374,11 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
         }
         const u32 start = incl - adeg;
         const u32 total = __shfl_sync(FULL, incl, 31);
-        u32 tv[2][SW_UNROLL];
-        int rv[2][SW_UNROLL];
-        auto issue = [&](int buf, u32 c0) {
+        // two register-resident batches (named, never indexed at run time, so
+        // they stay in registers and the column loads stay in flight)
+        u32 tvA[SW_UNROLL], tvB[SW_UNROLL];
+        int rvA[SW_UNROLL], rvB[SW_UNROLL];
+        auto issue = [&](u32 (&tv)[SW_UNROLL], int (&rv)[SW_UNROLL], u32 c0) {
 #pragma unroll
             for (int u = 0; u < SW_UNROLL; u++) {
                 const u32 p = c0 + (u32)(u * 32 + lane);
@@ -360,11 +390,11 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
                 }
                 const u64 rlo = __shfl_sync(FULL, lo, r);
                 const u32 rs = __shfl_sync(FULL, start, r);
-                rv[buf][u] = p < total ? r : -1;
-                tv[buf][u] = p < total ? __ldg(tgt + rlo + (p - rs)) : 0u;
+                rv[u] = p < total ? r : -1;
+                tv[u] = p < total ? __ldg(tgt + rlo + (p - rs)) : 0u;
             }
         };
-        if (total) issue(0, 0);
+        if (total) issue(tvA, rvA, 0);
         // fluid-to-history swap in registers, push value, counters
         double pv = 0.0;
         if (sel) {
@@ -396,16 +426,22 @@ __global__ void __launch_bounds__(SW_NT) k_sweep(SweepArgs<FT> a) {
             }
         }
         // scatter, one batch of 32*SW_UNROLL edges in flight ahead of the reds
-        int buf = 0;
-        for (u32 c0 = 0; c0 < total; c0 += 32 * SW_UNROLL) {
-            if (c0 + 32 * SW_UNROLL < total) issue(buf ^ 1, c0 + 32 * SW_UNROLL);
+        auto scatter = [&](const u32 (&tv)[SW_UNROLL], const int (&rv)[SW_UNROLL]) {
 #pragma unroll
             for (int u = 0; u < SW_UNROLL; u++) {
-                const int r = rv[buf][u];
+                const int r = rv[u];
                 const FT v = __shfl_sync(FULL, pvf, r < 0 ? 0 : r);
-                if (r >= 0) push_one(F, a.Fw, hot_acc, a.nhot, tv[buf][u], v);
+                if (r >= 0) push_one(F, a.Fw, hot_acc, a.nhot, tv[u], v);
             }
-            buf ^= 1;
+        };
+        constexpr u32 STEP = 32 * SW_UNROLL;
+        for (u32 c0 = 0; c0 < total; c0 += 2 * STEP) {
+            // batch A (in flight) is scattered while batch B loads, then the roles swap
+            if (c0 + STEP < total) issue(tvB, rvB, c0 + STEP);
+            scatter(tvA, rvA);
+            if (c0 + STEP >= total) break;
+            if (c0 + 2 * STEP < total) issue(tvA, rvA, c0 + 2 * STEP);
+            scatter(tvB, rvB);
         }
         f_cur = f_nx;
         lo_cur = lo_nx;
@@ -684,6 +720,9 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
         r.sweeps = (int64_t)c->sweeps;
         r.residual = residual;
         r.theta = theta_used;
+        u64 tns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+        r.t_ns = (int64_t)tns;
     }
     c->trace_len += 1;
     // theta schedule
@@ -755,6 +794,8 @@ __global__ void k_encode_targets(const u32 *__restrict__ tgt, long long m, const
         out[k] = s == 0xFFFFFFFFu ? t : (HOT_FLAG | s);
     }
 }
+
+int abs_sum_async(long long n, const void *x, int fp32, double *d_out, cudaStream_t st);  // fr_util.cu
 
 }  // namespace fr
 
@@ -1081,10 +1122,11 @@ static int reset_ctl(fr_solver *s, cudaStream_t st) {
     return FR_OK;
 }
 
-static int read_stats(fr_solver *s, cudaStream_t st, fr_solve_stats *h) {
-    SolveCtl c;
-    FR_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof(c), cudaMemcpyDeviceToHost, st));
+static int read_stats(fr_solver *s, cudaStream_t st, fr_solve_stats *h, double *exact = nullptr) {
+    static thread_local SolveCtl c;
+    FR_CUDA(cudaMemcpyAsync(&c, s->ctl, offsetof(SolveCtl, seg_next), cudaMemcpyDeviceToHost, st));
     FR_CUDA(cudaStreamSynchronize(st));
+    if (exact) *exact = c.exact;
     if (h) {
         h->diffusions = (int64_t)c.diffusions;
         h->elementary_steps = (int64_t)c.steps;
@@ -1103,11 +1145,12 @@ extern "C" int fr_solver_run(fr_solver *s, void *stream, fr_solve_stats *h_stats
     FR_TRY(reset_ctl(s, st));
     FR_CUDA(cudaGraphLaunch(s->exec, st));
     FR_CUDA(cudaGetLastError());
+    // exact sum |F| after the loop (the stopping rule of engine.py:290-293),
+    // stream-ordered into the control block; one host sync for all stats
+    FR_TRY(abs_sum_async(s->n, s->fp32 ? (void *)s->af.F : (void *)s->ad.F, s->fp32, &s->ctl->exact, st));
     fr_solve_stats hs;
-    FR_TRY(read_stats(s, st, &hs));
-    // exact check of the stopping rule (engine.py:290-293)
     double exact = 0.0;
-    FR_TRY(fr_abs_sum(s->n, s->fp32 ? (void *)s->af.F : (void *)s->ad.F, s->fp32, &exact, stream));
+    FR_TRY(read_stats(s, st, &hs, &exact));
     hs.residual = exact;
     if (h_stats) *h_stats = hs;
     const double thr = s->cfg.target_error * (1.0 - s->cfg.damping);

@@ -2,6 +2,10 @@
 // single-node diffusion step.
 #include <math.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "fr_common.cuh"
 
 namespace fr {
@@ -69,6 +73,41 @@ int reduce_grid(long long n) {
     return (int)(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
+// Persistent reduction scratch, one buffer per (device, stream): the L1 sums
+// run every solve, and a stream-ordered malloc/free per call showed up as
+// tens-of-milliseconds stalls in the solve timeline.  Never freed (a few KB).
+static std::mutex g_scratch_mu;
+static std::map<std::pair<int, cudaStream_t>, double *> g_scratch;
+static constexpr size_t SCRATCH_DOUBLES = 8192;
+
+int reduce_scratch(cudaStream_t st, double **out) {
+    int dev = 0;
+    FR_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    auto key = std::make_pair(dev, st);
+    auto it = g_scratch.find(key);
+    if (it == g_scratch.end()) {
+        double *p = nullptr;
+        FR_CUDA(cudaMalloc(&p, sizeof(double) * SCRATCH_DOUBLES));
+        it = g_scratch.emplace(key, p).first;
+    }
+    *out = it->second;
+    return FR_OK;
+}
+
+// sum |x| into the device double *d_out, stream-ordered, no host sync.
+int abs_sum_async(long long n, const void *x, int fp32, double *d_out, cudaStream_t st) {
+    double *part;
+    FR_TRY(reduce_scratch(st, &part));
+    const int g = reduce_grid(n);
+    if ((size_t)g + 1 > SCRATCH_DOUBLES) { set_error("reduction scratch too small"); return FR_ERR_ARG; }
+    if (fp32) k_abs_partials<float><<<g, RED_NT, 0, st>>>(n, (const float *)x, part);
+    else k_abs_partials<double><<<g, RED_NT, 0, st>>>(n, (const double *)x, part);
+    k_sum_parts<<<1, RED_NT, 0, st>>>(part, g, d_out);
+    FR_CUDA(cudaGetLastError());
+    return FR_OK;
+}
+
 }  // namespace fr
 
 using namespace fr;
@@ -88,15 +127,11 @@ extern "C" int fr_abs_sum(int64_t n, const void *d_x, int32_t x_fp32, double *h_
     if (n < 0 || (n > 0 && !d_x) || !h_sum) { set_error("fr_abs_sum: bad arguments"); return FR_ERR_ARG; }
     if (n == 0) { *h_sum = 0.0; return FR_OK; }
     cudaStream_t st = (cudaStream_t)stream;
-    Scratch scratch(st);
-    const int g = reduce_grid(n);
     double *part;
-    FR_TRY(scratch.alloc(&part, (size_t)g + 1));
-    if (x_fp32) k_abs_partials<float><<<g, RED_NT, 0, st>>>(n, (const float *)d_x, part);
-    else k_abs_partials<double><<<g, RED_NT, 0, st>>>(n, (const double *)d_x, part);
-    k_sum_parts<<<1, RED_NT, 0, st>>>(part, g, part + g);
-    FR_CUDA(cudaGetLastError());
-    FR_CUDA(cudaMemcpyAsync(h_sum, part + g, sizeof(double), cudaMemcpyDeviceToHost, st));
+    FR_TRY(reduce_scratch(st, &part));
+    double *d_out = part + SCRATCH_DOUBLES - 1;
+    FR_TRY(abs_sum_async(n, d_x, x_fp32, d_out, st));
+    FR_CUDA(cudaMemcpyAsync(h_sum, d_out, sizeof(double), cudaMemcpyDeviceToHost, st));
     FR_CUDA(cudaStreamSynchronize(st));
     return FR_OK;
 }
@@ -104,16 +139,14 @@ extern "C" int fr_abs_sum(int64_t n, const void *d_x, int32_t x_fp32, double *h_
 extern "C" int fr_normalize(int64_t n, const double *d_history, double *d_rank, double *h_total, void *stream) {
     if (n < 1 || !d_history || !d_rank) { set_error("fr_normalize: bad arguments"); return FR_ERR_ARG; }
     cudaStream_t st = (cudaStream_t)stream;
-    Scratch scratch(st);
-    const int g = reduce_grid(n);
     double *part;
-    FR_TRY(scratch.alloc(&part, (size_t)g + 1));
-    k_abs_partials<double><<<g, RED_NT, 0, st>>>(n, d_history, part);
-    k_sum_parts<<<1, RED_NT, 0, st>>>(part, g, part + g);
-    k_scale<<<g, RED_NT, 0, st>>>(n, d_history, part + g, d_rank);
+    FR_TRY(reduce_scratch(st, &part));
+    double *d_total = part + SCRATCH_DOUBLES - 1;
+    FR_TRY(abs_sum_async(n, d_history, 0, d_total, st));
+    k_scale<<<reduce_grid(n), RED_NT, 0, st>>>(n, d_history, d_total, d_rank);
     FR_CUDA(cudaGetLastError());
     if (h_total) {
-        FR_CUDA(cudaMemcpyAsync(h_total, part + g, sizeof(double), cudaMemcpyDeviceToHost, st));
+        FR_CUDA(cudaMemcpyAsync(h_total, d_total, sizeof(double), cudaMemcpyDeviceToHost, st));
         FR_CUDA(cudaStreamSynchronize(st));
     }
     return FR_OK;
