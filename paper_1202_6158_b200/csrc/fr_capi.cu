@@ -40,6 +40,36 @@ int device_info(DeviceInfo *out) {
     return FR_OK;
 }
 
+int pool_alloc(void **p, size_t bytes, cudaStream_t st) {
+    static std::mutex mu;
+    static bool configured[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice", __FILE__, __LINE__);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev < 64 && !configured[dev]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                unsigned long long thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            configured[dev] = true;
+        }
+    }
+    if (bytes == 0) bytes = 16;
+    e = cudaMallocAsync(p, bytes, st);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return cuda_fail(e, "cudaMallocAsync", __FILE__, __LINE__);
+    }
+    return FR_OK;
+}
+
+void pool_free(void *p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
 }  // namespace fr
 
 using namespace fr;
@@ -74,13 +104,11 @@ extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, 
     const size_t fsz = cfg->fluid_fp32 ? sizeof(float) : sizeof(double);
     do {
         cudaError_t e;
-        if ((e = cudaMallocAsync(&d_off, sizeof(int64_t) * (size_t)(n + 1), st)) != cudaSuccess ||
-            (e = cudaMallocAsync(&d_tgt, sizeof(uint32_t) * (size_t)(m > 0 ? m : 1), st)) != cudaSuccess ||
-            (e = cudaMallocAsync(&d_h, sizeof(double) * (size_t)n, st)) != cudaSuccess ||
-            (e = cudaMallocAsync(&d_f, fsz * (size_t)n, st)) != cudaSuccess) {
-            rc = cuda_fail(e, "cudaMallocAsync", __FILE__, __LINE__);
+        if ((rc = pool_alloc((void **)&d_off, sizeof(int64_t) * (size_t)(n + 1), st)) != FR_OK ||
+            (rc = pool_alloc((void **)&d_tgt, sizeof(uint32_t) * (size_t)(m > 0 ? m : 1), st)) != FR_OK ||
+            (rc = pool_alloc((void **)&d_h, sizeof(double) * (size_t)n, st)) != FR_OK ||
+            (rc = pool_alloc(&d_f, fsz * (size_t)n, st)) != FR_OK)
             break;
-        }
         if ((e = cudaMemcpyAsync(d_off, h_offsets, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice, st)) !=
                 cudaSuccess ||
             (m > 0 && (e = cudaMemcpyAsync(d_tgt, h_targets, sizeof(uint32_t) * (size_t)m, cudaMemcpyHostToDevice,
@@ -100,10 +128,10 @@ extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, 
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) rc = cuda_fail(e, "sync", __FILE__, __LINE__);
     } while (0);
     if (s) fr_solver_destroy(s);
-    cudaFreeAsync(d_off, st);
-    cudaFreeAsync(d_tgt, st);
-    cudaFreeAsync(d_h, st);
-    cudaFreeAsync(d_f, st);
+    pool_free(d_off, st);
+    pool_free(d_tgt, st);
+    pool_free(d_h, st);
+    pool_free(d_f, st);
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
     return rc;

@@ -38,6 +38,13 @@ struct DeviceInfo {
 };
 int device_info(DeviceInfo *out);
 
+// Stream-ordered allocations from the device's default pool.  The pool keeps
+// freed memory reserved (release threshold = max), so the multi-GB solver
+// buffers of repeated create/destroy cycles (the host-buffer entry point)
+// are recycled instead of being re-mapped by cudaMalloc/cudaFree each call.
+int pool_alloc(void **p, size_t bytes, cudaStream_t st);
+void pool_free(void *p, cudaStream_t st);
+
 // Stream-ordered scratch allocation; freed in the destructor on the same stream.
 struct Scratch {
     cudaStream_t stream;
@@ -45,17 +52,14 @@ struct Scratch {
     int count = 0;
     explicit Scratch(cudaStream_t s) : stream(s) {}
     ~Scratch() {
-        for (int i = count - 1; i >= 0; i--) cudaFreeAsync(ptrs[i], stream);
+        for (int i = count - 1; i >= 0; i--) pool_free(ptrs[i], stream);
     }
     template <typename T>
     int alloc(T **p, size_t elems) {
         size_t bytes = elems * sizeof(T);
         if (bytes == 0) bytes = 16;
-        cudaError_t e = cudaMallocAsync((void **)p, bytes, stream);
-        if (e != cudaSuccess) {
-            *p = nullptr;
-            return cuda_fail(e, "cudaMallocAsync(scratch)", __FILE__, __LINE__);
-        }
+        int rc = pool_alloc((void **)p, bytes, stream);
+        if (rc != FR_OK) return rc;
         ptrs[count++] = *p;
         return FR_OK;
     }

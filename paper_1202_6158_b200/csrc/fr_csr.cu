@@ -337,15 +337,31 @@ __global__ void __launch_bounds__(256) k_csr_squeeze(long long n, const u64 *__r
     }
 }
 
-__global__ void k_count_in_degree(const u32 *__restrict__ tgt, long long m, u64 *__restrict__ indeg) {
+// In-degree counting.  Zipf in-degree hubs receive a large share of all
+// increments and one address serialises in its L2 slice, so every counter is
+// spread over INDEG_COPIES copies in separate regions (copy = warp % copies),
+// summed afterwards.
+static constexpr int INDEG_COPIES = 8;
+
+__global__ void k_count_in_degree(const u32 *__restrict__ tgt, long long m, long long n, u32 *__restrict__ cnt) {
     const int lane = threadIdx.x & 31;
+    const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long base = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < m;
-         base += nwarps * 32) {
+    u32 *__restrict__ copy = cnt + (size_t)(gw % INDEG_COPIES) * (size_t)n;
+    for (long long base = gw * 32; base < m; base += nwarps * 32) {
         const long long e = base + lane;
         const u32 key = e < m ? ld_stream_u32(tgt + e) : NO_KEY;
         const u32 grp = __match_any_sync(0xffffffffu, key);
-        if (key != NO_KEY && lane == __ffs(grp) - 1) atomicAdd(indeg + key, (u64)__popc(grp));
+        if (key != NO_KEY && lane == __ffs(grp) - 1) atomicAdd(copy + key, (u32)__popc(grp));
+    }
+}
+
+__global__ void k_sum_copies(const u32 *__restrict__ cnt, long long n, u64 *__restrict__ indeg) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        u64 s = 0;
+#pragma unroll
+        for (int c = 0; c < INDEG_COPIES; c++) s += cnt[(size_t)c * (size_t)n + i];
+        indeg[i] = s;
     }
 }
 
@@ -464,8 +480,13 @@ extern "C" int fr_in_degree(int64_t n, int64_t m, const uint32_t *d_targets, int
     cudaStream_t st = (cudaStream_t)stream;
     DeviceInfo di;
     FR_TRY(device_info(&di));
-    FR_CUDA(cudaMemsetAsync(d_in_degree, 0, sizeof(int64_t) * (size_t)n, st));
-    if (m > 0) k_count_in_degree<<<di.sms * 8, 256, 0, st>>>(d_targets, m, reinterpret_cast<u64 *>(d_in_degree));
+    if (n == 0) return FR_OK;
+    Scratch scratch(st);
+    u32 *cnt;
+    FR_TRY(scratch.alloc(&cnt, (size_t)n * INDEG_COPIES));
+    FR_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u32) * (size_t)n * INDEG_COPIES, st));
+    if (m > 0) k_count_in_degree<<<di.sms * 8, 256, 0, st>>>(d_targets, m, n, cnt);
+    k_sum_copies<<<di.sms * 8, 256, 0, st>>>(cnt, n, reinterpret_cast<u64 *>(d_in_degree));
     FR_CUDA(cudaGetLastError());
     return FR_OK;
 }

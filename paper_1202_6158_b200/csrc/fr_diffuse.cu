@@ -807,6 +807,7 @@ struct fr_solver {
     int fp32;
     int sel_grid, sweep_grid, thread_grid, warp_grid, block_grid, fold_grid;
     u32 nhot, nslots;
+    cudaStream_t stream;  // creation stream (allocations and frees are ordered on it)
     SolveCtl *ctl;
     fr_trace_row *trace;
     long long trace_cap;
@@ -948,7 +949,7 @@ static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long
     FR_CUDA(cudaMemsetAsync(node_slot, 0xFF, sizeof(u32) * (size_t)n, st));
     const size_t cap = (size_t)want_hot + (size_t)want_warm;
     if (cap == 0) return FR_OK;
-    FR_CUDA(cudaMalloc(&s->slot_node, sizeof(u32) * cap));
+    FR_TRY(pool_alloc((void **)&s->slot_node, sizeof(u32) * cap, st));
     u32 nhot = 0, nwarm = 0;
     FR_CUDA(cudaMemsetAsync(d_count, 0, sizeof(u32), st));
     k_collect_class<<<g, 256, 0, st>>>(indeg, n, tau_hot, LLONG_MAX, 0, (u32)want_hot, s->slot_node, node_slot, d_count);
@@ -963,8 +964,8 @@ static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long
     if (nwarm > (u32)want_warm) nwarm = (u32)want_warm;
     const u32 nslots = nhot + nwarm;
     if (nslots == 0) return FR_OK;
-    FR_CUDA(cudaMalloc(&s->tgt_enc, sizeof(u32) * (size_t)m));
-    FR_CUDA(cudaMalloc(&s->fw_buf, sizeof(FT) * (size_t)nslots));
+    FR_TRY(pool_alloc((void **)&s->tgt_enc, sizeof(u32) * (size_t)m, st));
+    FR_TRY(pool_alloc(&s->fw_buf, sizeof(FT) * (size_t)nslots, st));
     FR_CUDA(cudaMemsetAsync(s->fw_buf, 0, sizeof(FT) * (size_t)nslots, st));
     k_encode_targets<<<g, 256, 0, st>>>(a.tgt, m, node_slot, s->tgt_enc);
     FR_CUDA(cudaGetLastError());
@@ -1019,11 +1020,13 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     }
     // queues: a selected node lands in exactly one bin
     const long long n = s->n, m = s->m;
-    const long long cap0 = n;
-    const long long cap1 = std::min<long long>(n, m / ((long long)a.t0 + 1) + 1);
+    // the fused path only queues hub rows; the binned path needs all three bins
+    const bool binned = c.kernel_path == 1;
+    const long long cap0 = binned ? n : 0;
+    const long long cap1 = binned ? std::min<long long>(n, m / ((long long)a.t0 + 1) + 1) : 0;
     const long long cap2 = std::min<long long>(n, m / (long long)a.t2 + 1);
-    FR_CUDA(cudaMalloc(&s->qnode_buf, sizeof(u32) * (size_t)(cap0 + cap1 + cap2 + 3)));
-    FR_CUDA(cudaMalloc(&s->qval_buf, sizeof(FT) * (size_t)(cap0 + cap1 + cap2 + 3)));
+    FR_TRY(pool_alloc(&s->qnode_buf, sizeof(u32) * (size_t)(cap0 + cap1 + cap2 + 3), st));
+    FR_TRY(pool_alloc(&s->qval_buf, sizeof(FT) * (size_t)(cap0 + cap1 + cap2 + 3), st));
     u32 *qn = (u32 *)s->qnode_buf;
     FT *qv = (FT *)s->qval_buf;
     a.qnode[0] = qn;
@@ -1042,8 +1045,8 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     const long long wtiles = ((n + 31) / 32 + SW_NT / 32 - 1) / (SW_NT / 32);
     if (s->sweep_grid > wtiles) s->sweep_grid = (int)std::max<long long>(1, wtiles);
     const int P = std::max(s->sel_grid, s->sweep_grid);
-    FR_CUDA(cudaMalloc(&s->parts, sizeof(double) * 3 * (size_t)P));
-    FR_CUDA(cudaMalloc(&s->parts64, sizeof(u64) * 3 * (size_t)P));
+    FR_TRY(pool_alloc((void **)&s->parts, sizeof(double) * 3 * (size_t)P, st));
+    FR_TRY(pool_alloc((void **)&s->parts64, sizeof(u64) * 3 * (size_t)P, st));
     a.part_mass = s->parts;
     a.part_abs = s->parts + P;
     a.part_max = s->parts + 2 * P;
@@ -1095,14 +1098,14 @@ extern "C" int fr_solver_create(int64_t n, int64_t m, const int64_t *d_offsets, 
     s->cfg = *cfg;
     s->fp32 = cfg->fluid_fp32 ? 1 : 0;
     s->trace_cap = trace_cap > 0 ? trace_cap : 0;
+    s->stream = (cudaStream_t)stream;
     int rc = FR_OK;
     do {
-        if (cudaMalloc(&s->ctl, sizeof(SolveCtl)) != cudaSuccess) { rc = cuda_fail(cudaGetLastError(), "cudaMalloc(ctl)", __FILE__, __LINE__); break; }
+        if ((rc = pool_alloc((void **)&s->ctl, sizeof(SolveCtl), (cudaStream_t)stream)) != FR_OK) break;
         if (s->trace_cap &&
-            cudaMalloc(&s->trace, sizeof(fr_trace_row) * (size_t)s->trace_cap) != cudaSuccess) {
-            rc = cuda_fail(cudaGetLastError(), "cudaMalloc(trace)", __FILE__, __LINE__);
+            (rc = pool_alloc((void **)&s->trace, sizeof(fr_trace_row) * (size_t)s->trace_cap, (cudaStream_t)stream)) !=
+                FR_OK)
             break;
-        }
         // all setup work is ordered on the caller's stream (its inputs may still be in flight there)
         rc = s->fp32 ? setup<float>(s, s->af, d_offsets, d_targets, d_score_weight, d_fluid, d_history,
                                     (cudaStream_t)stream)
@@ -1249,15 +1252,18 @@ extern "C" int fr_solver_destroy(fr_solver *s) {
     if (!s) return FR_OK;
     if (s->exec) cudaGraphExecDestroy(s->exec);
     if (s->graph) cudaGraphDestroy(s->graph);
-    cudaFree(s->ctl);
-    cudaFree(s->trace);
-    cudaFree(s->qnode_buf);
-    cudaFree(s->qval_buf);
-    cudaFree(s->parts);
-    cudaFree(s->parts64);
-    cudaFree(s->tgt_enc);
-    cudaFree(s->slot_node);
-    cudaFree(s->fw_buf);
+    // stream-ordered frees on the creation stream (callers destroy a solver
+    // only after the work that uses it has completed)
+    cudaStream_t st = s->stream;
+    pool_free(s->ctl, st);
+    pool_free(s->trace, st);
+    pool_free(s->qnode_buf, st);
+    pool_free(s->qval_buf, st);
+    pool_free(s->parts, st);
+    pool_free(s->parts64, st);
+    pool_free(s->tgt_enc, st);
+    pool_free(s->slot_node, st);
+    pool_free(s->fw_buf, st);
     delete s;
     return FR_OK;
 }
