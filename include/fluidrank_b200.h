@@ -142,6 +142,9 @@ typedef struct fr_solver_config {
     int32_t hot_slots;        /* fused path: pushes into the hot_slots highest in-degree
                                  nodes are summed per block in shared memory first
                                  (0 = default 2048, max 2048; -1 = off)             */
+    double degree_exponent;   /* FR_SELECT_SWEEP score = |f| * (out_degree + 1)^-degree_exponent
+                                 (0 = |f|, the reference sweep; 1 = the op2 weight of
+                                 sched.py:131-138; PAPER sec. 4.3 ALGO-OP2)          */
     int32_t warm_slots;       /* fused path: pushes into the next warm_slots highest
                                  in-degree nodes go to a compact L2-resident array that
                                  is folded back into F after every sweep

@@ -508,22 +508,24 @@ int fro_run_seq(int64_t n, const int64_t *off, const uint32_t *tgt, const int64_
 int fro_run_psweep(int64_t n, const int64_t *off, const uint32_t *tgt, double d, double target_error,
                    int policy, double decay, int64_t max_sweeps, int signed_, double *fluid,
                    double *history, fro_trace_row *trace, int64_t trace_cap, double *rank_out,
-                   fro_run_result *res)
+                   fro_run_result *res, const double *weight /* score multiplier (op/op2) or NULL */)
 {
     double threshold = target_error * (1.0 - d);
     int64_t diffusions = 0, steps = 0, sweeps = 0, tlen = 0;
     int64_t *sel = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
     double *sent = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
     double theta = 0.0, residual = pw_sum(fluid, n, signed_);
-    for (int64_t i = 0; i < n; i++) { double v = fabs(fluid[i]); if (v > theta) theta = v; }
+    for (int64_t i = 0; i < n; i++) { double v = fabs(fluid[i]) * (weight ? weight[i] : 1.0); if (v > theta) theta = v; }
     trace_push(trace, trace_cap, &tlen, steps, diffusions, residual, d);
     while (residual > threshold && (max_sweeps < 0 || sweeps < max_sweeps)) {
         int64_t ns = 0;
-        double mass = 0.0, absorbed = 0.0;
+        double mass = 0.0, absorbed = 0.0, mx = 0.0;
         for (int64_t i = 0; i < n; i++) {
             double f = fluid[i], a = fabs(f);
+            double sc = weight ? a * weight[i] : a;
             mass += a;
-            if (f != 0.0 && a >= theta) {
+            if (sc > mx) mx = sc;
+            if (f != 0.0 && sc >= theta) {
                 fluid[i] = 0.0;
                 history[i] += f;
                 sel[ns] = i;
@@ -541,7 +543,9 @@ int fro_run_psweep(int64_t n, const int64_t *off, const uint32_t *tgt, double d,
         diffusions += ns;
         sweeps++;
         residual = mass - absorbed;
-        if (ns == 0 || policy == 1) theta *= decay;
+        if (policy == 1) theta *= decay;
+        if (ns == 0 && mx > 0.0)
+            while (theta > mx) theta *= decay;
         trace_push(trace, trace_cap, &tlen, steps, diffusions, residual, d);
     }
     residual = pw_sum(fluid, n, signed_);

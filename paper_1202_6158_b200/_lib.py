@@ -44,7 +44,7 @@ class SolverConfig(ctypes.Structure):
                 ("fluid_fp32", ctypes.c_int32), ("thread_max_degree", ctypes.c_int32),
                 ("block_min_degree", ctypes.c_int32), ("seed", ctypes.c_uint32),
                 ("kernel_path", ctypes.c_int32), ("hot_slots", ctypes.c_int32),
-                ("warm_slots", ctypes.c_int32)]
+                ("degree_exponent", ctypes.c_double), ("warm_slots", ctypes.c_int32)]
 
 
 class TraceRow(ctypes.Structure):

@@ -86,6 +86,7 @@ struct SweepArgs {
     long long max_sweeps;
     long long max_diffusions;
     double d, thr, decay, rand_frac;
+    float beta;  // degree exponent: score = |f| * (out_degree + 1)^-beta (0: plain |f|)
     u32 t0, t2;  // deg <= t0 -> thread bin; deg >= t2 -> block bin
     int select, policy;
     u32 seed;
@@ -95,6 +96,11 @@ struct SweepArgs {
     int in_graph;
     cudaGraphConditionalHandle cond;
 };
+
+// (deg + 1)^-beta on the SFU; the score only orders nodes, so float precision suffices
+__device__ __forceinline__ double deg_weight(float beta, unsigned long long deg) {
+    return (double)exp2f(-beta * __log2f((float)deg + 1.0f));
+}
 
 __device__ __forceinline__ u64 hmix(u64 z) {
     z += 0x9E3779B97F4A7C15ull;
@@ -113,7 +119,9 @@ __global__ void __launch_bounds__(SEL_NT) k_mass_partials(SweepArgs<FT> a, int g
     for (long long i = blockIdx.x * (long long)SEL_NT + threadIdx.x; i < a.n; i += (long long)gridDim.x * SEL_NT) {
         const double af = fabs((double)a.F[i]);
         mass += af;
-        mx = fmax(mx, a.weight ? af * a.weight[i] : af);
+        double score = a.weight ? af * a.weight[i] : af;
+        if (a.beta != 0.0f) score = af * deg_weight(a.beta, a.off[i + 1] - a.off[i]);
+        mx = fmax(mx, score);
     }
     const double bm = block_sum<SEL_NT>(mass, sm);
     const double bx = block_max<SEL_NT>(mx, sm);
@@ -346,7 +354,8 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
         const u32 deg = (u32)(hi - lo);
         const FT f = f_cur;
         const double af = fabs((double)f);
-        const double score = (a.weight && valid) ? af * a.weight[i] : af;
+        double score = (a.weight && valid) ? af * a.weight[i] : af;
+        if (a.beta != 0.0f) score = af * deg_weight(a.beta, deg);
         mx = fmax(mx, score);
         bool sel;
         if (a.select == FR_SELECT_PER) sel = true;
@@ -494,7 +503,8 @@ __global__ void __launch_bounds__(SEL_NT) k_select(SweepArgs<FT> a) {
                 const FT f = a.F[i];
                 const double af = fabs((double)f);
                 mass += af;
-                const double score = a.weight ? af * a.weight[i] : af;
+                double score = a.weight ? af * a.weight[i] : af;
+                if (a.beta != 0.0f) score = af * deg_weight(a.beta, a.off[i + 1] - a.off[i]);
                 mx = fmax(mx, score);
                 bool sel;
                 if (a.select == FR_SELECT_PER) sel = true;
@@ -1009,6 +1019,9 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.policy = c.policy;
     a.seed = c.seed;
     a.path = c.kernel_path == 1 ? PATH_BINNED : PATH_FUSED;
+    a.beta = (float)c.degree_exponent;
+    // op2 (1/(out+1), sched.py:131-138) is the exponent 1: no weight array needed
+    if (c.select == FR_SELECT_OP2 && a.weight == nullptr) a.beta = 1.0f;
     {
         // tuning knobs for experiments (tools/prof_solver.py); defaults measured on config 5
         const char *e1 = getenv("FR_SEGS"), *e2 = getenv("FR_CHUNK");
@@ -1088,8 +1101,8 @@ extern "C" int fr_solver_create(int64_t n, int64_t m, const int64_t *d_offsets, 
         set_error("fr_solver_create: unknown select rule or theta policy");
         return FR_ERR_ARG;
     }
-    if ((cfg->select == FR_SELECT_OP || cfg->select == FR_SELECT_OP2) && !d_score_weight) {
-        set_error("fr_solver_create: op/op2 need per-node score weights");
+    if (cfg->select == FR_SELECT_OP && !d_score_weight) {
+        set_error("fr_solver_create: op needs per-node score weights 1/((in+1)(out+1))");
         return FR_ERR_ARG;
     }
     fr_solver *s = new fr_solver();

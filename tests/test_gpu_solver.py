@@ -258,3 +258,20 @@ def test_host_buffer_entry_point_with_hubs(cuda, oracle):
                                              rank.ctypes.data, ctypes.byref(stats)))
         ref = oracle.run_seq(off, tgt, 0.85, 1e-11, "sweep").rank
         assert l1(rank, ref) <= 1e-9
+
+
+@pytest.mark.parametrize("beta", [0.5, 1.0])
+@pytest.mark.parametrize("path", ["fused", "binned"])
+def test_degree_exponent_sweep(cuda, oracle, beta, path):
+    """Degree-scaled sweep score |f|(out+1)^-beta (PAPER sec. 4.3) converges to the same rank."""
+    src, dst = oracle.gen_edges(oracle.web_config(12.0), 50_000, 23)
+    off, tgt, _ = oracle.csr_build(50_000, src, dst, clean=True)
+    g = graph_from(cuda, off, tgt)
+    sched = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9, degree_exponent=beta, kernel_path=path)
+    rank, trace = cuda.run(g, cuda.DiffusionParams(target_error=1e-10), sched)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-12, "sweep").rank
+    assert l1(rank, ref) <= 1e-9
+    # the oracle's restatement of the same schedule does the same amount of work
+    deg = np.diff(off).astype(np.float64)
+    p = oracle.run_psweep(off, tgt, 0.85, 1e-10, policy=1, decay=0.9, weight=(deg + 1) ** -beta)
+    assert abs(trace.rows[-1].elementary_steps - p.elementary_steps) <= 0.15 * p.elementary_steps
