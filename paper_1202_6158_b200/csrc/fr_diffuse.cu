@@ -237,6 +237,9 @@ static constexpr int SW_PF = FR_SW_PF;  // L2 prefetch distance in tiles
 static constexpr int SW_UNROLL = FR_SW_UNROLL;
 
 
+#ifndef FR_TAKE_SUB
+#define FR_TAKE_SUB 1
+#endif
 __device__ __forceinline__ double take_fluid(double *p) {
     return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
 }
@@ -370,8 +373,16 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
         FT sent = (FT)0;
         double h_old = 0.0;
         if (sel) {
+#if FR_TAKE_SUB
+            // take exactly the fluid already loaded: a fire-and-forget
+            // subtraction (fluid pushed here since the load stays in F for
+            // the next sweep), so nothing below waits on a round trip
+            sent = f;
+            red_add(F + i, -f);
+#else
             sent = take_fluid(F + i);
             h_old = a.H[i];
+#endif
         }
         // compacted edge space of the active rows of this tile
         const u32 adeg = act ? deg : 0u;
@@ -390,7 +401,11 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
         auto issue = [&](u32 (&tv)[SW_UNROLL], int (&rv)[SW_UNROLL], u32 c0) {
 #pragma unroll
             for (int u = 0; u < SW_UNROLL; u++) {
-                const u32 p = c0 + (u32)(u * 32 + lane);
+                // lanes past the end re-read the last column (same line, no
+                // extra traffic): an unconditional load lands straight in its
+                // register, a predicated one forced a copy that waited on it
+                const u32 p0 = c0 + (u32)(u * 32 + lane);
+                const u32 p = p0 < total ? p0 : total - 1;
                 int r = 0;
 #pragma unroll
                 for (int s2 = 16; s2 > 0; s2 >>= 1) {
@@ -399,8 +414,8 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
                 }
                 const u64 rlo = __shfl_sync(FULL, lo, r);
                 const u32 rs = __shfl_sync(FULL, start, r);
-                rv[u] = p < total ? r : -1;
-                tv[u] = p < total ? __ldg(tgt + rlo + (p - rs)) : 0u;
+                rv[u] = p0 < total ? r : -1;
+                tv[u] = __ldg(tgt + rlo + (p - rs));
             }
         };
         if (total) issue(tvA, rvA, 0);
@@ -408,7 +423,11 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
         double pv = 0.0;
         if (sel) {
             const double as = fabs((double)sent);
+#if FR_TAKE_SUB
+            red_add(a.H + i, (double)sent);
+#else
             a.H[i] = h_old + (double)sent;
+#endif
             nsel++;
             if (deg == 0) {
                 absorbed += as;  // dangling: all of it leaves (PAPER sec. 3.3)
