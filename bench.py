@@ -198,24 +198,27 @@ def run_reference(args, world, rank):
 
 
 # ------------------------------------------------------------------ GPU arm
-def algorithmic_bytes(n, sweeps, diffusions, edges, hub_edges, fp32):
+def algorithmic_bytes(n, sweeps, diffusions, edges, hub_edges, fp32, narrow=False):
     """Algorithmic (compulsory) bytes of the fused sweep over one solve.
 
-    k_sweep, per sweep:       every node's fluid (8 B, 4 for fp32) + row offset (8 B)
+    k_sweep, per sweep:       every node's fluid (8 B, 4 for fp32) + row offset (8 B; 4 B
+                              for the solver's narrow copy when m < 2^32 and n < 2^31)
              per diffusion:   fluid write-back of the take (8/4 B) + history read+write (16 B)
              per pushed edge: column index (4 B) + the target's fluid value (8/4 B),
                               counted once per edge as in SpMV accounting
     k_push_block (hubs), per hub edge: 4 + 8/4 B.
     """
     fb = 4 if fp32 else 8
+    ob = 4 if narrow else 8
     own_edges = edges - hub_edges
-    sweep_b = sweeps * n * (fb + 8) + diffusions * (fb + 16) + own_edges * (4 + fb)
+    sweep_b = sweeps * n * (fb + ob) + diffusions * (fb + 16) + own_edges * (4 + fb)
     hub_b = hub_edges * (4 + fb)
     return sweep_b, hub_b
 
 
-BYTES_PER_EDGE_DOC = ("12 B per pushed edge (4 B column index + 8 B target fluid), plus 16 B per node per sweep "
-                      "(fluid + row offset scan) and 24 B per diffusion (take write-back + history r/w)")
+BYTES_PER_EDGE_DOC = ("12 B per pushed edge (4 B column index + 8 B target fluid), plus 12 B per node per sweep "
+                      "(8 B fluid + 4 B narrow row offset scan; 16 B when m >= 2^32) and 24 B per diffusion "
+                      "(take write-back + history r/w)")
 
 
 def run_ours(args, world, rank, local):
@@ -310,7 +313,9 @@ def run_ours(args, world, rank, local):
     kms, kl = solver.kernel_ms, solver.kernel_launches
     peak, peak_kind = load_peaks()
     if args.path == "fused":
-        sweep_b, hub_b = algorithmic_bytes(n, pst.sweeps, pst.diffusions, pst.elementary_steps, pst.hub_edges, fp32)
+        narrow = L < (1 << 32) and n < (1 << 31)  # the solver's narrow row-offset copy (fr_diffuse.cu setup)
+        sweep_b, hub_b = algorithmic_bytes(n, pst.sweeps, pst.diffusions, pst.elementary_steps, pst.hub_edges, fp32,
+                                           narrow)
         classes = {"k_sweep": (kms[0], kl[0], sweep_b), "k_push_block": (kms[3], kl[3], hub_b)}
     else:
         fb = 4 if fp32 else 8

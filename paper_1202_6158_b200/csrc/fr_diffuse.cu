@@ -29,6 +29,7 @@
 #include <cstddef>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "fr_common.cuh"
@@ -69,6 +70,7 @@ struct SweepArgs {
     FT *F;
     double *H;
     const u64 *off;
+    const u32 *off32;      // narrow copy of off when m < 2^32 and n < 2^31 (fused path), else null
     const u32 *tgt;
     const double *weight;  // score multiplier (op/op2) or null
     SolveCtl *ctl;
@@ -259,11 +261,16 @@ __device__ __forceinline__ u32 warp_sum_u32(u32 v) { return __reduce_add_sync(0x
 //     SW_UNROLL independent column loads in flight per lane, then
 //     red.global.add of sent*d/deg into F;
 //   * hub rows (deg >= t2) are queued for the block-per-node kernel.
-template <typename FT>
 #ifndef FR_SW_MINB
 #define FR_SW_MINB 4
 #endif
+// WIDE = false: 32-bit node / tile indices and the narrow row offsets (off32)
+// -- fewer registers and instructions per tile, half the offset traffic.
+template <typename FT, bool WIDE>
 __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
+    using OT = typename std::conditional<WIDE, u64, u32>::type;  // row offsets
+    using IT = typename std::conditional<WIDE, long long, u32>::type;  // node / tile indices
+    const OT *__restrict__ offp = WIDE ? (const OT *)a.off : (const OT *)a.off32;
     __shared__ double red_sm[SW_NT / 32];
     __shared__ u64 red_sm64[SW_NT / 32];
     __shared__ FT hot_acc[HOT_SLOTS];
@@ -275,7 +282,8 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
     const double keep_frac = 1.0 - a.d;
     double absorbed = 0.0, mx = 0.0;
     u64 steps = 0, nsel = 0, hsteps = 0;
-    const long long ntiles = (a.n + 31) >> 5;
+    const IT ntiles = (IT)((a.n + 31) >> 5);
+    const IT nn = (IT)a.n;
     const u32 *__restrict__ tgt = a.tgt;
     FT *__restrict__ F = a.F;
     hot_clear(hot_acc, a.nhot, SW_NT);
@@ -289,22 +297,23 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
     // chunks reach the minimum DRAM traffic, free-running warps ~1.8x it).
     const int SW_SEGS = a.segs;
     const u32 SW_CHUNK = a.chunk;
-    const long long seg_tiles = (ntiles + SW_SEGS - 1) / SW_SEGS;
+    const IT seg_tiles = (ntiles + SW_SEGS - 1) / SW_SEGS;
     int seg = (int)((blockIdx.x * (SW_NT / 32) + (threadIdx.x >> 5)) % SW_SEGS), misses = 0;
-    long long chunk_end = 0;
+    IT chunk_end = 0;
     // the next chunk is reserved one chunk ahead, so the counter's atomic
     // round trip overlaps the current chunk's work
     unsigned long long pend = 0;
     auto issue_grab = [&]() {
         if (lane == 0) pend = atomicAdd(&a.ctl->seg_next[seg * SEG_PAD], (unsigned long long)SW_CHUNK);
     };
-    auto grab = [&](long long &t) -> bool {
+    auto grab = [&](IT &t) -> bool {
         for (;;) {
             const unsigned long long k = __shfl_sync(FULL, pend, 0);
-            const long long s0 = (long long)seg * seg_tiles;
-            const long long s1 = s0 + seg_tiles < ntiles ? s0 + seg_tiles : ntiles;
-            if (s0 + (long long)k < s1) {
-                t = s0 + (long long)k;
+            // segments past the last tile are empty (s1 == s0; never wraps)
+            const IT s0 = (IT)seg * seg_tiles < ntiles ? (IT)seg * seg_tiles : ntiles;
+            const IT s1 = s0 + seg_tiles < ntiles ? s0 + seg_tiles : ntiles;
+            if (k < (unsigned long long)(s1 - s0)) {
+                t = s0 + (IT)k;
                 chunk_end = t + SW_CHUNK < s1 ? t + SW_CHUNK : s1;
                 misses = 0;
                 issue_grab();
@@ -316,43 +325,43 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
         }
     };
     issue_grab();
-    long long tile = 0;
+    IT tile = 0;
     bool have = grab(tile);
     // software pipeline: fluid and row offsets of the next tile are in flight
     // while the current tile is processed
     FT f_cur = (FT)0;
-    u64 lo_cur = 0, end_cur = 0;
-    auto load_tile = [&](long long t, FT &fo, u64 &loo, u64 &endo) {
-        const long long b = t << 5, i = b + lane;
-        const bool v = i < a.n;
-        loo = a.off[v ? i : a.n];
-        endo = lane == 31 ? a.off[b + 32 < a.n ? b + 32 : a.n] : 0ull;
+    OT lo_cur = 0, end_cur = 0;
+    auto load_tile = [&](IT t, FT &fo, OT &loo, OT &endo) {
+        const IT b = t << 5, i = b + lane;
+        const bool v = i < nn;
+        loo = offp[v ? i : nn];
+        endo = lane == 31 ? offp[b + 32 < nn ? b + 32 : nn] : (OT)0;
         fo = v ? F[i] : (FT)0;
     };
     if (have) load_tile(tile, f_cur, lo_cur, end_cur);
     while (have) {
-        long long nxt = tile + 1;
+        IT nxt = tile + 1;
         const bool have_nx = nxt < chunk_end ? true : grab(nxt);
         FT f_nx = (FT)0;
-        u64 lo_nx = 0, end_nx = 0;
+        OT lo_nx = 0, end_nx = 0;
         if (have_nx) load_tile(nxt, f_nx, lo_nx, end_nx);
         {
             // warm L2 with the fluid and offsets of a tile further ahead in the chunk
             // (no registers held), so the register prefetch above hits L2
-            const long long pf = tile + SW_PF;
+            const IT pf = tile + SW_PF;
             if (pf < chunk_end && (lane & 15) == 0) {
-                const long long j = (pf << 5) + lane;
-                if (j < a.n) {
+                const IT j = (pf << 5) + lane;
+                if (j < nn) {
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(F + j));
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.off + j));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(offp + j));
                 }
             }
         }
 
-        const long long i = (tile << 5) + lane;
-        const bool valid = i < a.n;
-        const u64 lo = lo_cur;
-        u64 hi = __shfl_down_sync(FULL, lo, 1);
+        const IT i = (tile << 5) + lane;
+        const bool valid = i < nn;
+        const OT lo = lo_cur;
+        OT hi = __shfl_down_sync(FULL, lo, 1);
         if (lane == 31) hi = end_cur;
         const u32 deg = (u32)(hi - lo);
         const FT f = f_cur;
@@ -412,7 +421,7 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
                     const u32 v = __shfl_sync(FULL, start, r + s2);
                     if (v <= p) r += s2;
                 }
-                const u64 rlo = __shfl_sync(FULL, lo, r);
+                const OT rlo = __shfl_sync(FULL, lo, r);
                 const u32 rs = __shfl_sync(FULL, start, r);
                 rv[u] = p0 < total ? r : -1;
                 tv[u] = __ldg(tgt + rlo + (p - rs));
@@ -831,6 +840,11 @@ int abs_sum_async(long long n, const void *x, int fp32, double *d_out, cudaStrea
 using namespace fr;
 
 // ====================================================================== host side
+template <typename FT>
+static void *sweep_kernel(const SweepArgs<FT> &a) {
+    return a.off32 ? (void *)k_sweep<FT, false> : (void *)k_sweep<FT, true>;
+}
+
 struct fr_solver {
     long long n, m;
     int fp32;
@@ -844,6 +858,7 @@ struct fr_solver {
     double *parts;
     u64 *parts64;
     u32 *tgt_enc;      // fused path: column indices with slotted targets encoded
+    u32 *off32;        // fused path: narrow row offsets (m < 2^32, n < 2^31), else null
     u32 *slot_node;
     void *fw_buf;
     fr_solver_config cfg;
@@ -894,7 +909,7 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
     if (a.path == PATH_FUSED) {
         // sweep -> hub pushes -> finalize -> (guarded) exact mass -> (guarded) check
         cudaGraphNode_t n_sw, n_hub, n_fold, n_fin, n_m, n_chk;
-        FR_TRY(add_kernel<FT>(body, &n_sw, nullptr, 0, (void *)k_sweep<FT>, s->sweep_grid, SW_NT, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_sw, nullptr, 0, sweep_kernel(a), s->sweep_grid, SW_NT, args_a));
         FR_TRY(add_kernel<FT>(body, &n_hub, &n_sw, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
         FR_TRY(add_kernel<FT>(body, &n_fold, &n_hub, 1, (void *)k_fold<FT>, s->fold_grid, 256, args_a));
         FR_TRY(add_kernel<FT>(body, &n_fin, &n_fold, 1, (void *)k_finalize<FT>, 1, FIN_NT, args_ans));
@@ -910,6 +925,11 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
     }
     FR_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
     return FR_OK;
+}
+
+__global__ void k_narrow_offsets(const u64 *__restrict__ off, long long n1, u32 *__restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n1; i += (long long)gridDim.x * blockDim.x)
+        out[i] = (u32)off[i];
 }
 
 template <typename FT>
@@ -1073,7 +1093,14 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     s->thread_grid = occupancy_grid<FT>((void *)k_push_thread<FT>, 256, di.sms);
     s->warp_grid = occupancy_grid<FT>((void *)k_push_warp<FT>, 256, di.sms);
     s->block_grid = occupancy_grid<FT>((void *)k_push_block<FT>, BLK_NT, di.sms);
-    s->sweep_grid = occupancy_grid<FT>((void *)k_sweep<FT>, SW_NT, di.sms);
+    a.off32 = nullptr;
+    if (a.path == PATH_FUSED && m < (1ll << 32) && n < (1ll << 31)) {
+        FR_TRY(pool_alloc((void **)&s->off32, sizeof(u32) * (size_t)(n + 1), st));
+        k_narrow_offsets<<<di.sms * 8, 256, 0, st>>>(a.off, n + 1, s->off32);
+        FR_CUDA(cudaGetLastError());
+        a.off32 = s->off32;
+    }
+    s->sweep_grid = occupancy_grid<FT>(sweep_kernel(a), SW_NT, di.sms);
     const long long wtiles = ((n + 31) / 32 + SW_NT / 32 - 1) / (SW_NT / 32);
     if (s->sweep_grid > wtiles) s->sweep_grid = (int)std::max<long long>(1, wtiles);
     const int P = std::max(s->sel_grid, s->sweep_grid);
@@ -1220,7 +1247,8 @@ static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve
     while (!stop) {
         // kernel classes: 0 select/sweep, 1 thread-bin push, 2 warp-bin push, 3 block-bin push, 4 finalize
         FR_CUDA(cudaEventRecord(ev[0], st));
-        if (fused) k_sweep<FT><<<s->sweep_grid, SW_NT, 0, st>>>(a);
+        if (fused && a.off32) k_sweep<FT, false><<<s->sweep_grid, SW_NT, 0, st>>>(a);
+        else if (fused) k_sweep<FT, true><<<s->sweep_grid, SW_NT, 0, st>>>(a);
         else k_select<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[1], st));
         if (!fused) k_push_thread<FT><<<s->thread_grid, 256, 0, st>>>(a);
@@ -1294,6 +1322,7 @@ extern "C" int fr_solver_destroy(fr_solver *s) {
     pool_free(s->parts, st);
     pool_free(s->parts64, st);
     pool_free(s->tgt_enc, st);
+    pool_free(s->off32, st);
     pool_free(s->slot_node, st);
     pool_free(s->fw_buf, st);
     delete s;
