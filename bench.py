@@ -253,7 +253,7 @@ def run_ours(args, world, rank, local):
     sched = fr.make_scheduler("sweep", policy=args.policy, sweep_decay=args.decay,
                               thread_max_degree=args.thread_max, block_min_degree=args.block_min,
                               kernel_path=args.path, hot_slots=args.hot_slots,
-                              warm_slots=args.warm_slots, degree_exponent=args.beta)
+                              warm_slots=args.warm_slots, degree_exponent=args.beta, edge_frac=args.edge_frac)
     state = fr.init(g, params, fluid_dtype=torch.float32 if fp32 else torch.float64)
     solver = fr.Solver(g, state, sched, params, trace_cap=1 << 16)
     rank_out = torch.empty(n, dtype=torch.float64, device=dev)
@@ -351,7 +351,8 @@ def run_ours(args, world, rank, local):
     plain = None
     if args.beta != 0.0 and not args.no_plain:
         sched0 = fr.make_scheduler("sweep", policy=args.policy, sweep_decay=args.decay, kernel_path=args.path,
-                                   hot_slots=args.hot_slots, warm_slots=args.warm_slots, degree_exponent=0.0)
+                                   hot_slots=args.hot_slots, warm_slots=args.warm_slots, degree_exponent=0.0,
+                                   edge_frac=args.edge_frac)
         st0 = fr.init(g, params, fluid_dtype=torch.float32 if fp32 else torch.float64)
         sol0 = fr.Solver(g, st0, sched0, params, trace_cap=16)
         sol0.run()
@@ -455,6 +456,7 @@ def run_ours(args, world, rank, local):
             "config": {"workload": w["name"], "n": n, "edges": L, "edge_slots_drawn": slots,
                        "duplicates_dropped": dups, "self_loops_dropped": loops, "damping": w["damping"],
                        "target_error": w["target"], "policy": args.policy, "decay": args.decay,
+                       "edge_frac": args.edge_frac if args.policy == "adaptive" else None,
                        "kernel_path": args.path, "hot_slots": args.hot_slots, "warm_slots": args.warm_slots,
                        "degree_exponent": args.beta,
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
@@ -490,12 +492,14 @@ def main():
     ap.add_argument("--config", type=int, default=5, choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=0, help="override node count (scaled workload)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--policy", default="geometric", choices=("exhaust", "geometric", "mass"))
-    ap.add_argument("--decay", type=float, default=0.9)
+    ap.add_argument("--policy", default="adaptive", choices=("exhaust", "geometric", "adaptive"))
+    ap.add_argument("--decay", type=float, default=0.7, help="theta decay per sweep (adaptive: nominal)")
+    ap.add_argument("--edge-frac", type=float, default=0.15,
+                    help="adaptive theta: target edges pushed per sweep as a fraction of m")
     ap.add_argument("--path", default="fused", choices=("fused", "binned"))
     ap.add_argument("--hot-slots", type=int, default=0, help="0 default (2048), -1 off")
     ap.add_argument("--warm-slots", type=int, default=0, help="0 default (2^21), -1 off")
-    ap.add_argument("--beta", type=float, default=0.5, help="degree exponent of the sweep score")
+    ap.add_argument("--beta", type=float, default=0.65, help="degree exponent of the sweep score")
     ap.add_argument("--fluid", default="fp64", choices=("fp64", "fp32"))
     ap.add_argument("--thread-max", type=int, default=0)
     ap.add_argument("--block-min", type=int, default=0)

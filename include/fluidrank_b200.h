@@ -117,7 +117,8 @@ enum fr_select {
 enum fr_theta_policy {
     FR_THETA_EXHAUST = 0,   /* decay only after a sweep that finds nothing (sched.py:101-108) */
     FR_THETA_GEOMETRIC = 1, /* decay after every sweep (PAPER sec. 4.2)                       */
-    FR_THETA_MASS = 2       /* theta from the fused fluid-mass exponent histogram             */
+    FR_THETA_ADAPTIVE = 2   /* theta steered so a sweep pushes ~ edge_frac * m edges:
+                               theta *= decay * sqrt(pushed / (edge_frac * m)), clamped   */
 };
 
 typedef struct fr_solver_config {
@@ -125,7 +126,7 @@ typedef struct fr_solver_config {
     double target_error;      /* stop when residual <= target*(1-d)    */
     double decay;             /* theta decay factor (sched.py:79)      */
     double rand_frac;         /* FR_SELECT_RAND selection probability  */
-    double mass_frac;         /* FR_THETA_MASS: fluid mass per sweep   */
+    double edge_frac;         /* FR_THETA_ADAPTIVE: target pushed edges per sweep / m (<= 0: 0.2) */
     int64_t max_sweeps;       /* sweep budget (<= 0: 1e6)              */
     int64_t max_diffusions;   /* stop once this many diffusions ran (<= 0: none);
                                  required when damping == 1 (engine.py:256-257) */

@@ -503,13 +503,18 @@ int fro_run_seq(int64_t n, const int64_t *off, const uint32_t *tgt, const int64_
 /*                 (the reference sweep scheduler's rule, sched.py:101-108)  */
 /*   1 geometric : theta *= decay after every sweep (sec. 4.2,      */
 /*                 "scaling down the threshold progressively")               */
+/*   2 adaptive  : theta *= clamp(decay * sqrt(E / (edge_frac * m)),         */
+/*                 0.25, 1.5), E = edges pushed by the sweep (product rule,  */
+/*                 fr_diffuse.cu k_finalize)                                 */
 /* Used to check the GPU's sweep counters and as the schedule model.        */
 /* ------------------------------------------------------------------------ */
 int fro_run_psweep(int64_t n, const int64_t *off, const uint32_t *tgt, double d, double target_error,
                    int policy, double decay, int64_t max_sweeps, int signed_, double *fluid,
                    double *history, fro_trace_row *trace, int64_t trace_cap, double *rank_out,
-                   fro_run_result *res, const double *weight /* score multiplier (op/op2) or NULL */)
+                   fro_run_result *res, const double *weight /* score multiplier (op/op2) or NULL */,
+                   double edge_frac /* policy 2 target; <= 0: 0.2 */)
 {
+    const double edge_target = (edge_frac > 0.0 ? edge_frac : 0.2) * (double)(off[n] - off[0]);
     double threshold = target_error * (1.0 - d);
     int64_t diffusions = 0, steps = 0, sweeps = 0, tlen = 0;
     int64_t *sel = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
@@ -518,7 +523,7 @@ int fro_run_psweep(int64_t n, const int64_t *off, const uint32_t *tgt, double d,
     for (int64_t i = 0; i < n; i++) { double v = fabs(fluid[i]) * (weight ? weight[i] : 1.0); if (v > theta) theta = v; }
     trace_push(trace, trace_cap, &tlen, steps, diffusions, residual, d);
     while (residual > threshold && (max_sweeps < 0 || sweeps < max_sweeps)) {
-        int64_t ns = 0;
+        int64_t ns = 0, steps0 = steps;
         double mass = 0.0, absorbed = 0.0, mx = 0.0;
         for (int64_t i = 0; i < n; i++) {
             double f = fluid[i], a = fabs(f);
@@ -544,6 +549,11 @@ int fro_run_psweep(int64_t n, const int64_t *off, const uint32_t *tgt, double d,
         sweeps++;
         residual = mass - absorbed;
         if (policy == 1) theta *= decay;
+        if (policy == 2) {
+            double ratio = edge_target > 0.0 ? (double)(steps - steps0) / edge_target : 1.0;
+            double q = decay * sqrt(ratio > 1e-6 ? ratio : 1e-6);
+            theta *= q < 0.25 ? 0.25 : (q > 1.5 ? 1.5 : q);
+        }
         if (ns == 0 && mx > 0.0)
             while (theta > mx) theta *= decay;
         trace_push(trace, trace_cap, &tlen, steps, diffusions, residual, d);

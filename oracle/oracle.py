@@ -74,7 +74,7 @@ def lib():
         L.fro_run_seq.argtypes = [i64, P, P, P, f64, f64, i32, f64, i64, i64, i32, P, P,
                                   f64, i64, i64, P, i64, P, P]
         L.fro_run_psweep.restype = i32
-        L.fro_run_psweep.argtypes = [i64, P, P, f64, f64, i32, f64, i64, i32, P, P, P, i64, P, P, P]
+        L.fro_run_psweep.argtypes = [i64, P, P, f64, f64, i32, f64, i64, i32, P, P, P, i64, P, P, P, f64]
         L.fro_power_iterate.restype = i64
         L.fro_power_iterate.argtypes = [i64, P, P, P, i64, f64, P, f64, i64, i64, P, P, i64, P, P]
         _lib = L
@@ -215,7 +215,8 @@ def run_seq(off, tgt, damping=0.85, target_error=1e-8, kind="sweep", decay=0.5,
 
 
 def run_psweep(off, tgt, damping=0.85, target_error=1e-8, policy=0, decay=0.5,
-               teleport=None, max_sweeps=None, fluid=None, history=None, trace_cap=1 << 16, weight=None):
+               teleport=None, max_sweeps=None, fluid=None, history=None, trace_cap=1 << 16, weight=None,
+               edge_frac=0.2):
     """The product's data-parallel threshold sweep, restated sequentially."""
     n = off.size - 1
     off = np.ascontiguousarray(off, dtype=np.int64)
@@ -229,7 +230,7 @@ def run_psweep(off, tgt, damping=0.85, target_error=1e-8, policy=0, decay=0.5,
     w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float64)
     lib().fro_run_psweep(n, _ptr(off), _ptr(tgt), damping, target_error, policy, decay,
                          -1 if max_sweeps is None else max_sweeps, int(signed), _ptr(fluid),
-                         _ptr(history), rows, trace_cap, _ptr(rank), ctypes.byref(res), _ptr(w))
+                         _ptr(history), rows, trace_cap, _ptr(rank), ctypes.byref(res), _ptr(w), edge_frac)
     return OracleRun(rank, history, fluid, res.residual, res.diffusions, res.elementary_steps,
                      res.sweeps, _trace_array(rows, res.trace_len))
 

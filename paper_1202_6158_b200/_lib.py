@@ -24,7 +24,7 @@ FR_ERR_NO_CONVERGENCE = 6
 FR_ERR_NO_DEVICE = 7
 
 SELECT = {"sweep": 0, "max": 1, "per": 2, "rand": 3, "op": 4, "op2": 5}
-POLICY = {"exhaust": 0, "geometric": 1, "mass": 2}
+POLICY = {"exhaust": 0, "geometric": 1, "adaptive": 2}
 
 
 class GenConfig(ctypes.Structure):
@@ -38,7 +38,7 @@ class GenConfig(ctypes.Structure):
 class SolverConfig(ctypes.Structure):
     _fields_ = [("damping", ctypes.c_double), ("target_error", ctypes.c_double),
                 ("decay", ctypes.c_double), ("rand_frac", ctypes.c_double),
-                ("mass_frac", ctypes.c_double), ("max_sweeps", ctypes.c_int64),
+                ("edge_frac", ctypes.c_double), ("max_sweeps", ctypes.c_int64),
                 ("max_diffusions", ctypes.c_int64),
                 ("select", ctypes.c_int32), ("policy", ctypes.c_int32),
                 ("fluid_fp32", ctypes.c_int32), ("thread_max_degree", ctypes.c_int32),

@@ -31,14 +31,14 @@ import torch
 from . import _lib
 
 KINDS = ("max", "rand", "per", "sweep", "op", "op2")
-POLICIES = ("exhaust", "geometric", "mass")
+POLICIES = ("exhaust", "geometric", "adaptive")
 
 
 class DeviceSchedule:
     """A selection rule plus its theta policy; consumed by engine.run."""
 
     def __init__(self, kind, seed=0, decay=0.5, policy="exhaust", rand_frac=0.25,
-                 mass_frac=0.5, thread_max_degree=0, block_min_degree=0, kernel_path="fused", hot_slots=0,
+                 edge_frac=0.2, thread_max_degree=0, block_min_degree=0, kernel_path="fused", hot_slots=0,
                  warm_slots=0, degree_exponent=0.0):
         if kind not in KINDS:
             raise ValueError(f"unknown scheduler kind {kind!r}; expected one of {KINDS}")
@@ -51,7 +51,9 @@ class DeviceSchedule:
         self.decay = float(decay)
         self.policy = policy
         self.rand_frac = float(rand_frac)
-        self.mass_frac = float(mass_frac)
+        if edge_frac <= 0:
+            raise ValueError(f"edge_frac must be > 0, got {edge_frac}")
+        self.edge_frac = float(edge_frac)
         self.thread_max_degree = int(thread_max_degree)
         self.block_min_degree = int(block_min_degree)
         if kernel_path not in ("fused", "binned"):
@@ -83,7 +85,7 @@ class DeviceSchedule:
         c.target_error = float(params.target_error)
         c.decay = self.decay
         c.rand_frac = self.rand_frac
-        c.mass_frac = self.mass_frac
+        c.edge_frac = self.edge_frac
         c.max_sweeps = int(max_sweeps or 0)
         c.max_diffusions = int(max_diffusions or 0)
         c.select = _lib.SELECT[self.kind]

@@ -275,3 +275,23 @@ def test_degree_exponent_sweep(cuda, oracle, beta, path):
     deg = np.diff(off).astype(np.float64)
     p = oracle.run_psweep(off, tgt, 0.85, 1e-10, policy=1, decay=0.9, weight=(deg + 1) ** -beta)
     assert abs(trace.rows[-1].elementary_steps - p.elementary_steps) <= 0.15 * p.elementary_steps
+
+
+@pytest.mark.parametrize("damping", [0.85, 0.99])
+@pytest.mark.parametrize("path", ["fused", "binned"])
+def test_adaptive_theta(cuda, oracle, damping, path):
+    """Adaptive theta (edges per sweep steered to edge_frac*m) converges to the same rank,
+    and its sweep/edge counts follow the oracle's restatement of the rule."""
+    src, dst = oracle.gen_edges(oracle.web_config(12.0), 50_000, 29)
+    off, tgt, _ = oracle.csr_build(50_000, src, dst, clean=True)
+    g = graph_from(cuda, off, tgt)
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.75, degree_exponent=0.65,
+                                kernel_path=path)
+    rank, trace = cuda.run(g, cuda.DiffusionParams(damping=damping, target_error=1e-10), sched)
+    ref = oracle.run_seq(off, tgt, damping, 1e-12, "sweep").rank
+    assert l1(rank, ref) <= 1e-9
+    deg = np.diff(off).astype(np.float64)
+    p = oracle.run_psweep(off, tgt, damping, 1e-10, policy=2, decay=0.75, weight=(deg + 1) ** -0.65,
+                          edge_frac=0.2)
+    assert abs(trace.rows[-1].elementary_steps - p.elementary_steps) <= 0.2 * p.elementary_steps
+    assert abs(trace.rows[-1].sweeps - p.sweeps) <= max(3, 0.2 * p.sweeps)

@@ -35,8 +35,8 @@ def test_parallel_sweep_agrees_with_sequential(oracle):
     src, dst = oracle.gen_edges(cfg, 3000, 9)
     off, tgt, _ = oracle.csr_build(3000, src, dst, clean=True)
     seq = oracle.run_seq(off, tgt, 0.85, 1e-10, "sweep")
-    for policy in (0, 1):
-        par = oracle.run_psweep(off, tgt, 0.85, 1e-10, policy=policy)
+    for policy in (0, 1, 2):  # exhaust, geometric, adaptive
+        par = oracle.run_psweep(off, tgt, 0.85, 1e-10, policy=policy, decay=0.75 if policy == 2 else 0.5)
         assert np.abs(par.rank - seq.rank).sum() <= 2e-10
         assert par.residual <= 1e-10 * 0.15
 

@@ -16,13 +16,14 @@ from paper_1202_6158_b200 import gen  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=100_000_000)
 ap.add_argument("--mean", type=float, default=16.0)
-ap.add_argument("--policy", default="geometric")
-ap.add_argument("--decay", type=float, default=0.9)
+ap.add_argument("--policy", default="adaptive")
+ap.add_argument("--edge-frac", type=float, default=0.15)
+ap.add_argument("--decay", type=float, default=0.7)
 ap.add_argument("--fluid", default="fp64")
 ap.add_argument("--path", default="fused")
 ap.add_argument("--hot-slots", type=int, default=0)
 ap.add_argument("--block-min", type=int, default=0)
-ap.add_argument("--beta", type=float, default=0.0)
+ap.add_argument("--beta", type=float, default=0.65)
 ap.add_argument("--warm-slots", type=int, default=0)
 ap.add_argument("--graph", action="store_true", help="run the CUDA-graph path instead")
 ap.add_argument("--local-frac", type=float, default=0.7)
@@ -34,7 +35,7 @@ params = fr.DiffusionParams(target_error=1e-9)
 state = fr.init(g, params, fluid_dtype=torch.float32 if args.fluid == "fp32" else torch.float64)
 solver = fr.Solver(g, state, fr.make_scheduler("sweep", policy=args.policy, sweep_decay=args.decay, kernel_path=args.path, hot_slots=args.hot_slots, warm_slots=args.warm_slots,
                                                      block_min_degree=args.block_min,
-                                                     degree_exponent=args.beta), params)
+                                                     degree_exponent=args.beta, edge_frac=args.edge_frac), params)
 t = time.perf_counter()
 st = solver.run(profiled=not args.graph)
 torch.cuda.synchronize()
