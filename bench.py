@@ -417,6 +417,31 @@ def run_ours(args, world, rank, local):
         sol99.close()
         del st99
 
+    # ---- batched personalized PageRank (BASELINE configs[3]): 1M-node web graph,
+    # 64 personalization vectors x 10 seeds, every column to L1 residual 1e-9
+    ppr = None
+    if not args.no_ppr:
+        g4, _ = gen.generate(gen.web_config(8.0), 1_000_000, args.seed)
+        seeds = fr.config4_seeds(g4.n, 64, 10, seed=args.seed)
+        pp = fr.BatchedPPR(g4, 64, 0.85, w["target"])
+        pp.solve(seeds)  # warm-up (graph instantiation)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rank4, st4, res4 = pp.solve(seeds)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t4 = reduce_max(e0.elapsed_time(e1), world) / 1000.0
+        colsum = float((rank4.sum(0) - 1.0).abs().max())
+        ppr = {"workload": "BASELINE configs[3]: N=1M web graph (mean out-degree 8, %d edges), 64 vectors x 10 "
+                           "seeds, d=0.85, each column to L1 residual 1e-9, n x 64 fp64 row-major state" % g4.edge_count,
+               "time_s": t4, "sweeps": st4.sweeps, "row_visits": st4.diffusions, "edge_visits": st4.elementary_steps,
+               "max_column_residual": max(res4), "max_column_sum_error": colsum, "decay": 0.6,
+               "timing": "one fr_ppr_init + fr_ppr_run + normalize, CUDA events"}
+        pp.close()
+        del rank4, g4
+        torch.cuda.empty_cache()
+
     # ---- end to end through the C ABI from pinned host buffers
     h_off = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
     h_tgt = torch.empty(L, dtype=torch.int32, pin_memory=True)
@@ -473,6 +498,7 @@ def run_ours(args, world, rank, local):
             "d099": d099,
             "plain_score_schedule": plain,
             "power_iteration": power,
+            "ppr": ppr,
             "roofline": roofline,
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "clocks": clocks,
@@ -506,6 +532,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-d099", action="store_true", help="skip the d=0.99 solve")
+    ap.add_argument("--no-ppr", action="store_true", help="skip the batched PPR (configs[3]) solve")
     ap.add_argument("--no-plain", action="store_true", help="skip the beta=0 comparison solve")
     ap.add_argument("--no-power", action="store_true", help="skip the power-iteration comparison")
     args = ap.parse_args()

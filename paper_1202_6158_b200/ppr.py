@@ -27,7 +27,7 @@ def config4_seeds(n, B=64, k=10, seed=0):
 class BatchedPPR:
     """fr_ppr_* handle: graph + (n x B) state, reusable across solves."""
 
-    def __init__(self, graph, B, damping=0.85, target_error=1e-9, decay=0.9, max_sweeps=0):
+    def __init__(self, graph, B, damping=0.85, target_error=1e-9, decay=0.6, max_sweeps=0):
         if not 1 <= B <= 64:
             raise ValueError(f"B must be in [1, 64], got {B}")
         dev = require_device()
@@ -73,7 +73,7 @@ class BatchedPPR:
             pass
 
 
-def personalized_pagerank(graph, seeds, damping=0.85, target_error=1e-9, decay=0.9):
+def personalized_pagerank(graph, seeds, damping=0.85, target_error=1e-9, decay=0.6):
     """Rank vectors (n x B) for B seed sets (B x k), one batched device solve."""
     seeds = np.asarray(seeds)
     p = BatchedPPR(graph, seeds.shape[0], damping, target_error, decay)
