@@ -149,7 +149,7 @@ typedef struct fr_solver_config {
     int32_t warm_slots;       /* fused path: pushes into the next warm_slots highest
                                  in-degree nodes go to a compact L2-resident array that
                                  is folded back into F after every sweep
-                                 (0 = default 2^21, -1 = off)                       */
+                                 (0 = default 2^19, max 2^24, -1 = off)             */
 } fr_solver_config;
 
 typedef struct fr_trace_row {
