@@ -100,9 +100,15 @@ struct SweepArgs {
     cudaGraphConditionalHandle cond;
 };
 
-// (deg + 1)^-beta on the SFU; the score only orders nodes, so float precision suffices
+// (deg + 1)^-beta on the SFU (two MUFU ops, no denormal fix-ups: deg + 1 >= 1
+// and the result is >= 2^-32 for beta <= 1); the score only orders nodes, so
+// float precision suffices.  Every kernel uses this one function, so the
+// selection is consistent between the sweep, the mass pass and the binned path.
 __device__ __forceinline__ double deg_weight(float beta, unsigned long long deg) {
-    return (double)exp2f(-beta * __log2f((float)deg + 1.0f));
+    float l, w;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"((float)deg + 1.0f));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(-beta * l));
+    return (double)w;
 }
 
 __device__ __forceinline__ u64 hmix(u64 z) {
@@ -239,6 +245,7 @@ __global__ void __launch_bounds__(256) k_fold(SweepArgs<FT> a) {
 static constexpr int SW_NT = FR_SW_NT;
 static constexpr int SW_PF = FR_SW_PF;  // L2 prefetch distance in tiles
 static constexpr int SW_UNROLL = FR_SW_UNROLL;
+static constexpr int DSC_TAB = 256;  // tabulated d/deg in k_sweep
 
 
 #ifndef FR_TAKE_SUB
@@ -295,6 +302,9 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
     const u32 *__restrict__ tgt = a.tgt;
     FT *__restrict__ F = a.F;
     hot_clear(hot_acc, a.nhot, SW_NT);
+    // d/deg for the common small degrees (bit-identical to the division below)
+    __shared__ double dsc_sm[DSC_TAB];
+    for (int q = threadIdx.x; q < DSC_TAB; q += SW_NT) dsc_sm[q] = q ? a.d / (double)q : 0.0;
     __syncthreads();
     // In-order scheduling: the tiles are split into SW_SEGS contiguous segments,
     // each with its own counter; a warp takes SW_CHUNK consecutive tiles of its
@@ -356,13 +366,12 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
         {
             // warm L2 with the fluid and offsets of a tile further ahead in the chunk
             // (no registers held), so the register prefetch above hits L2
+            // lanes 0, 1: the tile's two 128 B fluid lines (fp64), lane 2: its offsets
             const IT pf = tile + SW_PF;
-            if (pf < chunk_end && (lane & 15) == 0) {
-                const IT j = (pf << 5) + lane;
-                if (j < nn) {
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(F + j));
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(offp + j));
-                }
+            if (pf < chunk_end && lane < 3) {
+                const IT j = (pf << 5) + (lane & 1) * 16;
+                const void *pa = lane < 2 ? (const void *)(F + j) : (const void *)(offp + j);
+                if (j < nn) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
             }
         }
 
@@ -451,7 +460,7 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
             } else {
                 absorbed += as * keep_frac;
                 steps += deg;
-                pv = (double)sent * (a.d / (double)deg);  // sent*(d/deg), engine.py:321
+                pv = (double)sent * (deg < DSC_TAB ? dsc_sm[deg] : a.d / (double)deg);  // sent*(d/deg), engine.py:321
             }
         }
         const FT pvf = (FT)pv;
@@ -1355,7 +1364,7 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     {
         // tuning knobs for experiments (tools/prof_solver.py); defaults measured on config 5
         const char *e1 = getenv("FR_SEGS"), *e2 = getenv("FR_CHUNK");
-        a.segs = e1 ? atoi(e1) : 64;
+        a.segs = e1 ? atoi(e1) : 32;
         a.chunk = e2 ? (u32)atoi(e2) : 8u;
         if (a.segs < 1) a.segs = 1;
         if (a.segs > SW_MAX_SEGS) a.segs = SW_MAX_SEGS;
