@@ -273,12 +273,7 @@ __device__ __forceinline__ u32 warp_sum_u32(u32 v) { return __reduce_add_sync(0x
 #ifndef FR_SW_MINB
 #define FR_SW_MINB 4
 #endif
-#ifndef FR_PIPE_U0
-#define FR_PIPE_U0 1
-#endif
-#ifndef FR_SW_PIPE
-#define FR_SW_PIPE 0  // 1: tile-pipelined sweep for narrow graphs (k_sweep_pipe; measured no faster)
-#endif
+
 // WIDE = false: 32-bit node / tile indices and the narrow row offsets (off32)
 // -- fewer registers and instructions per tile, half the offset traffic.
 template <typename FT, bool WIDE>
@@ -510,278 +505,6 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
     const u64 bs = block_sum_u64<SW_NT>(steps, red_sm64);
     const u64 bn = block_sum_u64<SW_NT>(nsel, red_sm64);
     const u64 bh = block_sum_u64<SW_NT>(hsteps, red_sm64);
-    if (threadIdx.x == 0) {
-        a.part_hsteps[blockIdx.x] = bh;
-        a.part_abs[blockIdx.x] = ba;
-        a.part_max[blockIdx.x] = bx;
-        a.part_steps[blockIdx.x] = bs;
-        a.part_sel[blockIdx.x] = bn;
-        a.part_mass[blockIdx.x] = 0.0;
-    }
-}
-
-// Tile-pipelined variant of the narrow fused sweep.  The first column batch
-// of tile t is issued before tile t-1 is scattered, so its DRAM latency
-// overlaps the previous tile's reds instead of stalling the warp (it was the
-// largest stall of k_sweep).  Only that in-flight batch is carried across the
-// iteration in registers; the pending tile's row data (compacted start, row
-// offset, push value) sits in a per-warp shared-memory slot, where the later
-// batches of a long tile binary-search it.
-template <typename FT>
-__global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep_pipe(SweepArgs<FT> a) {
-    constexpr int U = SW_UNROLL;
-    constexpr int U0 = FR_PIPE_U0;  // width (x32) of the first batch carried across an iteration
-    struct RowSlot {
-        u32 start[32];
-        u32 lo[32];
-        FT pv[32];
-        int rv0[U0][32];  // row of each edge of the in-flight first batch (-1: none)
-    };
-    __shared__ double red_sm[SW_NT / 32];
-    __shared__ u64 red_sm64[SW_NT / 32];
-    __shared__ FT hot_acc[HOT_SLOTS];
-    __shared__ RowSlot rows_sm[SW_NT / 32][2];
-    __shared__ u64 cnt_sm[SW_NT / 32][3];  // per warp: selected nodes, pushed edges, hub edges
-    __shared__ double theta_sm;
-    constexpr u32 FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const u32 *__restrict__ offp = a.off32;
-    // registers are the limit here (64 for 4 blocks/SM): warp counters live in
-    // shared memory, theta is re-read from it, the sweep index only on the rand path
-    double absorbed = 0.0, mx = 0.0;
-    if (lane < 3) cnt_sm[wid][lane] = 0;
-    if (threadIdx.x == 0) theta_sm = a.ctl->theta;
-    const u32 ntiles = (u32)((a.n + 31) >> 5);
-    const u32 nn = (u32)a.n;
-    const u32 *__restrict__ tgt = a.tgt;
-    FT *__restrict__ F = a.F;
-    hot_clear(hot_acc, a.nhot, SW_NT);
-    __syncthreads();
-    const int SW_SEGS = a.segs;
-    const u32 SW_CHUNK = a.chunk;
-    const u32 seg_tiles = (ntiles + SW_SEGS - 1) / SW_SEGS;
-    int seg = (int)((blockIdx.x * (SW_NT / 32) + wid) % SW_SEGS), misses = 0;
-    u32 chunk_end = 0;
-    u32 pend = 0;
-    auto issue_grab = [&]() {
-        // low half of the (zeroed) 64-bit segment counter: tile offsets < 2^32
-        if (lane == 0) pend = atomicAdd(reinterpret_cast<u32 *>(&a.ctl->seg_next[seg * SEG_PAD]), SW_CHUNK);
-    };
-    auto grab = [&](u32 &t) -> bool {
-        for (;;) {
-            const u32 k = __shfl_sync(FULL, pend, 0);
-            const u32 s0 = (u32)seg * seg_tiles < ntiles ? (u32)seg * seg_tiles : ntiles;
-            const u32 s1 = s0 + seg_tiles < ntiles ? s0 + seg_tiles : ntiles;
-            if (k < s1 - s0) {
-                t = s0 + k;
-                chunk_end = t + SW_CHUNK < s1 ? t + SW_CHUNK : s1;
-                misses = 0;
-                issue_grab();
-                return true;
-            }
-            seg = (seg + 1) % SW_SEGS;
-            if (++misses >= SW_SEGS) return false;
-            issue_grab();
-        }
-    };
-    issue_grab();
-    u32 tile = 0;
-    bool have = grab(tile);
-    FT f_cur = (FT)0;
-    u32 lo_cur = 0, end_cur = 0;
-    auto load_tile = [&](u32 t, FT &fo, u32 &loo, u32 &endo) {
-        const u32 b = t << 5, i = b + lane;
-        const bool v = i < nn;
-        loo = offp[v ? i : nn];
-        endo = lane == 31 ? offp[b + 32 < nn ? b + 32 : nn] : 0u;
-        fo = v ? F[i] : (FT)0;
-    };
-    if (have) load_tile(tile, f_cur, lo_cur, end_cur);
-    constexpr u32 STEP = 32 * U;
-    // first batch of the current tile, from lane-held row data; the row of
-    // each edge goes to the slot (only the column values stay in registers)
-    auto issue_reg = [&](u32 (&tv)[U0], RowSlot &S, u32 st, u32 l, u32 tot) {
-#pragma unroll
-        for (int u = 0; u < U0; u++) {
-            const u32 p0 = (u32)(u * 32 + lane);
-            const u32 p = p0 < tot ? p0 : tot - 1;  // unconditional load (see k_sweep)
-            int r = 0;
-#pragma unroll
-            for (int s2 = 16; s2 > 0; s2 >>= 1) {
-                const u32 v = __shfl_sync(FULL, st, r + s2);
-                if (v <= p) r += s2;
-            }
-            const u32 rlo = __shfl_sync(FULL, l, r);
-            const u32 rs = __shfl_sync(FULL, st, r);
-            tv[u] = __ldg(tgt + rlo + (p - rs));
-            S.rv0[u][lane] = p0 < tot ? r : -1;
-        }
-    };
-    // batch [c0, c0 + STEP) of a pending tile, from its shared-memory slot
-    auto issue_sm = [&](u32 (&tv)[U], int (&rv)[U], u32 c0, const RowSlot &S, u32 tot) {
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const u32 p0 = c0 + (u32)(u * 32 + lane);
-            const u32 p = p0 < tot ? p0 : tot - 1;
-            int r = 0;
-#pragma unroll
-            for (int s2 = 16; s2 > 0; s2 >>= 1)
-                if (S.start[r + s2] <= p) r += s2;
-            rv[u] = p0 < tot ? r : -1;
-            tv[u] = __ldg(tgt + S.lo[r] + (p - S.start[r]));
-        }
-    };
-    auto scatter = [&](const u32 (&tv)[U], const int (&rv)[U], const RowSlot &S) {
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int r = rv[u];
-            if (r >= 0) push_one(F, a.Fw, hot_acc, a.nhot, tv[u], S.pv[r]);
-        }
-    };
-    // scatter a pending tile: its first batch (in flight since the previous
-    // iteration), then the remaining batches ping-ponged as in k_sweep
-    constexpr u32 STEP0 = 32 * U0;
-    auto drain = [&](const u32 (&tv0)[U0], const RowSlot &S, u32 tot) {
-        if (!tot) return;
-        u32 tvA[U], tvB[U];
-        int rvA[U], rvB[U];
-        if (tot > STEP0) issue_sm(tvB, rvB, STEP0, S, tot);
-#pragma unroll
-        for (int u = 0; u < U0; u++) {
-            const int r = S.rv0[u][lane];
-            if (r >= 0) push_one(F, a.Fw, hot_acc, a.nhot, tv0[u], S.pv[r]);
-        }
-        for (u32 c0 = STEP0; c0 < tot; c0 += 2 * STEP) {
-            if (c0 + STEP < tot) issue_sm(tvA, rvA, c0 + STEP, S, tot);
-            scatter(tvB, rvB, S);
-            if (c0 + STEP >= tot) break;
-            if (c0 + 2 * STEP < tot) issue_sm(tvB, rvB, c0 + 2 * STEP, S, tot);
-            scatter(tvA, rvA, S);
-        }
-    };
-    // one iteration: select + take the current tile into (tvC, rvC, SC, totC),
-    // issue its first batch, then drain the pending tile (tvP, rvP, SP, totP)
-    auto body = [&](u32 (&tvC)[U0], RowSlot &SC, u32 &totC, const u32 (&tvP)[U0], const RowSlot &SP, u32 totP) {
-        u32 nxt = tile + 1;
-        const bool have_nx = nxt < chunk_end ? true : grab(nxt);
-        FT f_nx = (FT)0;
-        u32 lo_nx = 0, end_nx = 0;
-        if (have_nx) load_tile(nxt, f_nx, lo_nx, end_nx);
-        {
-            const u32 pf = tile + SW_PF;
-            if (pf < chunk_end && (lane & 15) == 0) {
-                const u32 j = (pf << 5) + lane;
-                if (j < nn) {
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(F + j));
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(offp + j));
-                }
-            }
-        }
-        const u32 i = (tile << 5) + lane;
-        const bool valid = i < nn;
-        const u32 lo = lo_cur;
-        u32 hi = __shfl_down_sync(FULL, lo, 1);
-        if (lane == 31) hi = end_cur;
-        const u32 deg = hi - lo;
-        const FT f = f_cur;
-        const double af = fabs((double)f);
-        double score = (a.weight && valid) ? af * a.weight[i] : af;
-        if (a.beta != 0.0f) score = af * deg_weight(a.beta, deg);
-        mx = fmax(mx, score);
-        bool sel;
-        if (a.select == FR_SELECT_PER) sel = true;
-        else if (a.select == FR_SELECT_RAND)
-            sel = (double)(hmix(((u64)a.seed << 40) ^ (a.ctl->sweeps << 32) ^ hmix((u64)i)) >> 11) * 0x1.0p-53 <
-                  a.rand_frac;
-        else sel = score >= theta_sm;
-        sel = sel && valid && f != (FT)0;
-        const bool big = deg >= a.t2;
-        const bool act = sel && !big && deg > 0;
-        double pv = 0.0;
-        if (sel) {
-            // take exactly the loaded fluid, fire-and-forget (see k_sweep)
-            red_add(F + i, -f);
-            red_add(a.H + i, (double)f);
-            if (deg == 0) {
-                absorbed += af;  // dangling: all of it leaves (PAPER sec. 3.3)
-            } else {
-                absorbed = fma(-af, a.d, absorbed + af);  // af * (1 - d)
-                pv = (double)f * (a.d / (double)deg);    // sent*(d/deg), engine.py:321
-            }
-        }
-        const FT pvf = (FT)pv;
-        const u32 adeg = act ? deg : 0u;
-        u32 incl = adeg;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 t = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const u32 start = incl - adeg;
-        const u32 total = __shfl_sync(FULL, incl, 31);
-        totC = total;
-        __syncwarp();  // SC was last read by the drain of two iterations ago
-        if (total) issue_reg(tvC, SC, start, lo, total);
-        {
-            // selected nodes, pushed edges (hub rows added below)
-            const u32 ns = __popc(__ballot_sync(FULL, sel));
-            if (lane == 0 && ns) {
-                cnt_sm[wid][0] += ns;
-                cnt_sm[wid][1] += total;
-            }
-        }
-        SC.start[lane] = start;
-        SC.lo[lane] = lo;
-        SC.pv[lane] = pvf;
-        // hubs -> block-per-node kernel
-        const bool hub = sel && big;
-        const u32 hmask = __ballot_sync(FULL, hub);
-        if (hmask) {
-            u32 hb = 0;
-            const int leader = __ffs(hmask) - 1;
-            if (lane == leader) hb = atomicAdd(&a.ctl->qcount[2], (u32)__popc(hmask));
-            hb = __shfl_sync(FULL, hb, leader);
-            if (hub) {
-                const u32 q = hb + __popc(hmask & ((1u << lane) - 1u));
-                a.qnode[2][q] = i;
-                a.qval[2][q] = pvf;
-                atomicAdd(&cnt_sm[wid][1], (u64)deg);
-                atomicAdd(&cnt_sm[wid][2], (u64)deg);
-            }
-        }
-        drain(tvP, SP, totP);
-        f_cur = f_nx;
-        lo_cur = lo_nx;
-        end_cur = end_nx;
-        tile = nxt;
-        have = have_nx;
-    };
-    // two named sets alternated by unrolling: a register copy of a batch whose
-    // loads are in flight would wait on them
-    u32 tvX[U0], tvY[U0];
-    u32 totX = 0, totY = 0;
-    RowSlot &SX = rows_sm[wid][0], &SY = rows_sm[wid][1];
-    while (have) {
-        body(tvX, SX, totX, tvY, SY, totY);
-        __syncwarp();
-        if (!have) {
-            drain(tvX, SX, totX);
-            break;
-        }
-        body(tvY, SY, totY, tvX, SX, totX);
-        __syncwarp();
-        if (!have) {
-            drain(tvY, SY, totY);
-            break;
-        }
-    }
-    __syncthreads();
-    hot_flush(a.Fw, hot_acc, a.nhot, SW_NT);
-    const double ba = block_sum<SW_NT>(absorbed, red_sm);
-    const double bx = block_max<SW_NT>(mx, red_sm);
-    const u64 bs = block_sum_u64<SW_NT>(lane == 0 ? cnt_sm[wid][1] : 0ull, red_sm64);
-    const u64 bn = block_sum_u64<SW_NT>(lane == 0 ? cnt_sm[wid][0] : 0ull, red_sm64);
-    const u64 bh = block_sum_u64<SW_NT>(lane == 0 ? cnt_sm[wid][2] : 0ull, red_sm64);
     if (threadIdx.x == 0) {
         a.part_hsteps[blockIdx.x] = bh;
         a.part_abs[blockIdx.x] = ba;
@@ -1153,8 +876,12 @@ using namespace fr;
 // ====================================================================== host side
 template <typename FT>
 static void *sweep_kernel(const SweepArgs<FT> &a) {
-    if (!a.off32) return (void *)k_sweep<FT, true>;
-    return FR_SW_PIPE ? (void *)k_sweep_pipe<FT> : (void *)k_sweep<FT, false>;
+    return a.off32 ? (void *)k_sweep<FT, false> : (void *)k_sweep<FT, true>;
+}
+template <typename FT>
+static void launch_sweep(const SweepArgs<FT> &a, int grid, cudaStream_t st) {
+    if (a.off32) k_sweep<FT, false><<<grid, SW_NT, 0, st>>>(a);
+    else k_sweep<FT, true><<<grid, SW_NT, 0, st>>>(a);
 }
 
 struct fr_solver {
@@ -1409,6 +1136,7 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
         FR_CUDA(cudaGetLastError());
         a.off32 = s->off32;
     }
+
     s->sweep_grid = occupancy_grid<FT>(sweep_kernel(a), SW_NT, di.sms);
     const long long wtiles = ((n + 31) / 32 + SW_NT / 32 - 1) / (SW_NT / 32);
     if (s->sweep_grid > wtiles) s->sweep_grid = (int)std::max<long long>(1, wtiles);
@@ -1556,9 +1284,7 @@ static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve
     while (!stop) {
         // kernel classes: 0 select/sweep, 1 thread-bin push, 2 warp-bin push, 3 block-bin push, 4 finalize
         FR_CUDA(cudaEventRecord(ev[0], st));
-        if (fused && a.off32 && FR_SW_PIPE) k_sweep_pipe<FT><<<s->sweep_grid, SW_NT, 0, st>>>(a);
-        else if (fused && a.off32) k_sweep<FT, false><<<s->sweep_grid, SW_NT, 0, st>>>(a);
-        else if (fused) k_sweep<FT, true><<<s->sweep_grid, SW_NT, 0, st>>>(a);
+        if (fused) launch_sweep<FT>(a, s->sweep_grid, st);
         else k_select<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[1], st));
         if (!fused) k_push_thread<FT><<<s->thread_grid, 256, 0, st>>>(a);
