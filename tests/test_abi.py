@@ -61,3 +61,38 @@ def test_product_does_not_import_oracle():
             "#", "\n#").split("\n#")[0] or True
         src = open(path).read()
         assert "import oracle" not in src and "from oracle" not in src, path
+
+
+def _c_layout(struct, fields, tmp_path):
+    """sizeof / offsetof of a header struct, from a tiny C program compiled with gcc."""
+    import subprocess
+    src = tmp_path / "layout.c"
+    body = "".join(f'printf("%zu ", offsetof({struct}, {f}));' for f in fields)
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "fluidrank_b200.h"\n'
+                   f'int main(void) {{ printf("%zu ", sizeof({struct})); {body} return 0; }}\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    return [int(x) for x in out]
+
+
+@pytest.mark.parametrize("name,struct", [("SolverConfig", "fr_solver_config"), ("SolveStats", "fr_solve_stats"),
+                                         ("TraceRow", "fr_trace_row"), ("GenConfig", "fr_gen_config")])
+def test_ctypes_structs_match_the_header(tmp_path, name, struct):
+    """The ctypes mirrors in _lib.py have the C layout (sizes and every field offset)."""
+    from paper_1202_6158_b200 import _lib
+    cls = getattr(_lib, name)
+    fields = [f[0] for f in cls._fields_]
+    c = _c_layout(struct, fields, tmp_path)
+    py = [ctypes.sizeof(cls)] + [getattr(cls, f).offset for f in fields]
+    assert c == py
+
+
+def test_integration_stub_matches_the_library():
+    """The ctypes stub shown in INTEGRATION.md declares the same struct layouts."""
+    from paper_1202_6158_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    ns = {"ctypes": ctypes}
+    exec(text[text.index("class SolverConfig"):text.index("_lib.fr_pagerank_host.argtypes")], ns)
+    for name in ("SolverConfig", "SolveStats"):
+        assert ns[name]._fields_ == getattr(_lib, name)._fields_, name
