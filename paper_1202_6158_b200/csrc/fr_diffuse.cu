@@ -239,6 +239,9 @@ __global__ void __launch_bounds__(256) k_fold(SweepArgs<FT> a) {
 #ifndef FR_SW_UNROLL
 #define FR_SW_UNROLL 2
 #endif
+#ifndef FR_PF_LANES
+#define FR_PF_LANES 3  // 5: also the history lines (measured neutral)
+#endif
 #ifndef FR_SW_PF
 #define FR_SW_PF 3
 #endif
@@ -361,11 +364,15 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
         {
             // warm L2 with the fluid and offsets of a tile further ahead in the chunk
             // (no registers held), so the register prefetch above hits L2
-            // lanes 0, 1: the tile's two 128 B fluid lines (fp64), lane 2: its offsets
+            // lanes 0, 1: the tile's two 128 B fluid lines (fp64), lane 2: its
+            // offsets, lanes 3, 4: its history lines (the history red.adds of
+            // the ~half of the nodes a sweep selects would otherwise miss L2)
             const IT pf = tile + SW_PF;
-            if (pf < chunk_end && lane < 3) {
+            if (pf < chunk_end && lane < FR_PF_LANES) {
                 const IT j = (pf << 5) + (lane & 1) * 16;
-                const void *pa = lane < 2 ? (const void *)(F + j) : (const void *)(offp + j);
+                const void *pa = lane < 2 ? (const void *)(F + j)
+                                 : lane == 2 ? (const void *)(offp + j)
+                                             : (const void *)(a.H + (pf << 5) + (lane - 3) * 16);
                 if (j < nn) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
             }
         }
@@ -1130,7 +1137,11 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     s->warp_grid = occupancy_grid<FT>((void *)k_push_warp<FT>, 256, di.sms);
     s->block_grid = occupancy_grid<FT>((void *)k_push_block<FT>, BLK_NT, di.sms);
     a.off32 = nullptr;
-    if (a.path == PATH_FUSED && m < (1ll << 32) && n < (1ll << 31)) {
+    // FR_FORCE_WIDE=1 keeps the 64-bit kernel on small graphs (tests of the
+    // m >= 2^32 / n >= 2^31 path, which no test-sized graph would take)
+    const char *fw = getenv("FR_FORCE_WIDE");
+    const bool force_wide = fw && fw[0] == '1';
+    if (a.path == PATH_FUSED && !force_wide && m < (1ll << 32) && n < (1ll << 31)) {
         FR_TRY(pool_alloc((void **)&s->off32, sizeof(u32) * (size_t)(n + 1), st));
         k_narrow_offsets<<<di.sms * 8, 256, 0, st>>>(a.off, n + 1, s->off32);
         FR_CUDA(cudaGetLastError());

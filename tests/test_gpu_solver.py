@@ -295,3 +295,30 @@ def test_adaptive_theta(cuda, oracle, damping, path):
                           edge_frac=0.2)
     assert abs(trace.rows[-1].elementary_steps - p.elementary_steps) <= 0.2 * p.elementary_steps
     assert abs(trace.rows[-1].sweeps - p.sweeps) <= max(3, 0.2 * p.sweeps)
+
+
+@pytest.mark.parametrize("fluid", ["fp64", "fp32"])
+def test_wide_index_kernel(cuda, oracle, monkeypatch, fluid):
+    """The 64-bit-offset sweep kernel (taken when m >= 2^32 or n >= 2^31) on a test-sized graph
+    (FR_FORCE_WIDE=1 skips the narrow offset copy): same rank, same work as the narrow kernel."""
+    monkeypatch.setenv("FR_FORCE_WIDE", "1")
+    src, dst = oracle.gen_edges(oracle.web_config(12.0), 200_000, 37)
+    off, tgt, _ = oracle.csr_build(200_000, src, dst, clean=True)
+    g = graph_from(cuda, off, tgt)
+    # fp32 fluid: a 1e-8 target (its stated rank tolerance is 1e-6); near 1e-10 the
+    # fp32 rounding floor makes the number of sweeps vary from run to run
+    fp32 = fluid == "fp32"
+    params = cuda.DiffusionParams(target_error=1e-8 if fp32 else 1e-10)
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65,
+                                edge_frac=0.15)
+    dtype = torch.float32 if fp32 else torch.float64
+    rank, trace = cuda.run(g, params, sched, fluid_dtype=dtype)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-12, "sweep").rank
+    tol = 1e-6 if fp32 else 1e-9
+    assert l1(rank, ref) <= tol
+    monkeypatch.delenv("FR_FORCE_WIDE")
+    rank2, trace2 = cuda.run(g, params, sched, fluid_dtype=dtype)
+    assert l1(rank2, ref) <= tol
+    if not fp32:
+        e1, e2 = trace.rows[-1].elementary_steps, trace2.rows[-1].elementary_steps
+        assert abs(e1 - e2) <= 0.15 * e2
