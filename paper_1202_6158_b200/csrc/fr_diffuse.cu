@@ -616,21 +616,29 @@ __global__ void __launch_bounds__(SEL_NT) k_select(SweepArgs<FT> a) {
 // ------------------------------------------------------------------ P: push kernels
 template <typename FT>
 __global__ void __launch_bounds__(256) k_push_thread(SweepArgs<FT> a) {
+    __shared__ FT hot_acc[HOT_SLOTS];
     const u32 cnt = a.ctl->qcount[0];
     const u32 *__restrict__ qn = a.qnode[0];
     const FT *__restrict__ qv = a.qval[0];
+    hot_clear(hot_acc, a.nhot, 256);
+    __syncthreads();
     for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
         const u32 node = qn[e];
         const FT v = qv[e];
         const u64 lo = a.off[node], hi = a.off[node + 1];
-        for (u64 k = lo; k < hi; k++) red_add(a.F + __ldg(a.tgt + k), v);
+        for (u64 k = lo; k < hi; k++) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + k), v);
     }
+    __syncthreads();
+    hot_flush(a.Fw, hot_acc, a.nhot, 256);
 }
 
 template <typename FT>
 __global__ void __launch_bounds__(256) k_push_warp(SweepArgs<FT> a) {
+    __shared__ FT hot_acc[HOT_SLOTS];
     const u32 cnt = a.ctl->qcount[1];
     const int lane = threadIdx.x & 31;
+    hot_clear(hot_acc, a.nhot, 256);
+    __syncthreads();
     const u32 nwarps = gridDim.x * (blockDim.x >> 5);
     const uint4 *tgt4 = reinterpret_cast<const uint4 *>(a.tgt);
     for (u32 e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nwarps) {
@@ -639,16 +647,18 @@ __global__ void __launch_bounds__(256) k_push_warp(SweepArgs<FT> a) {
         const u64 lo = a.off[node], hi = a.off[node + 1];
         const u64 a0 = min(hi, (lo + 3) & ~3ull);
         const u64 a1 = max(a0, hi & ~3ull);
-        if (lo + lane < a0) red_add(a.F + __ldg(a.tgt + lo + lane), v);
-        if (a1 + lane < hi) red_add(a.F + __ldg(a.tgt + a1 + lane), v);
+        if (lo + lane < a0) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + lo + lane), v);
+        if (a1 + lane < hi) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + a1 + lane), v);
         for (u64 q = (a0 >> 2) + lane; q < (a1 >> 2); q += 32) {
             const uint4 t = ld_stream_u4(tgt4 + q);
-            red_add(a.F + t.x, v);
-            red_add(a.F + t.y, v);
-            red_add(a.F + t.z, v);
-            red_add(a.F + t.w, v);
+            push_one(a.F, a.Fw, hot_acc, a.nhot, t.x, v);
+            push_one(a.F, a.Fw, hot_acc, a.nhot, t.y, v);
+            push_one(a.F, a.Fw, hot_acc, a.nhot, t.z, v);
+            push_one(a.F, a.Fw, hot_acc, a.nhot, t.w, v);
         }
     }
+    __syncthreads();
+    hot_flush(a.Fw, hot_acc, a.nhot, 256);
 }
 
 __device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
@@ -962,12 +972,14 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
         FR_TRY(add_kernel<FT>(body, &n_m, &n_fin, 1, (void *)k_mass_partials<FT>, s->sel_grid, SEL_NT, args_m1));
         FR_TRY(add_kernel<FT>(body, &n_chk, &n_m, 1, (void *)k_mass_check<FT>, 1, FIN_NT, args_an));
     } else {
-        cudaGraphNode_t n_sel, n_p[3], n_fin;
+        // select -> three push bins (concurrent) -> fold of the warm slots -> finalize
+        cudaGraphNode_t n_sel, n_p[3], n_fold, n_fin;
         FR_TRY(add_kernel<FT>(body, &n_sel, nullptr, 0, (void *)k_select<FT>, s->sel_grid, SEL_NT, args_a));
         FR_TRY(add_kernel<FT>(body, &n_p[0], &n_sel, 1, (void *)k_push_thread<FT>, s->thread_grid, 256, args_a));
         FR_TRY(add_kernel<FT>(body, &n_p[1], &n_sel, 1, (void *)k_push_warp<FT>, s->warp_grid, 256, args_a));
         FR_TRY(add_kernel<FT>(body, &n_p[2], &n_sel, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
-        FR_TRY(add_kernel<FT>(body, &n_fin, n_p, 3, (void *)k_finalize<FT>, 1, FIN_NT, args_an));
+        FR_TRY(add_kernel<FT>(body, &n_fold, n_p, 3, (void *)k_fold<FT>, s->fold_grid, 256, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_fin, &n_fold, 1, (void *)k_finalize<FT>, 1, FIN_NT, args_an));
     }
     FR_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
     return FR_OK;
@@ -1164,7 +1176,7 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.Fw = nullptr;
     a.nhot = 0;
     a.nslots = 0;
-    if (a.path == PATH_FUSED && m > 0) {
+    if (m > 0) {
         const int want_hot = c.hot_slots < 0 ? 0 : (c.hot_slots ? c.hot_slots : HOT_SLOTS);
         const long long want_warm = c.warm_slots < 0 ? 0 : (c.warm_slots ? c.warm_slots : (long long)WARM_DEFAULT);
         FR_TRY(prepare_slots(s, a, want_hot, want_warm, st));
@@ -1304,7 +1316,7 @@ static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve
         FR_CUDA(cudaEventRecord(ev[3], st));
         k_push_block<FT><<<s->block_grid, BLK_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[4], st));
-        if (fused) k_fold<FT><<<s->fold_grid, 256, 0, st>>>(a);
+        k_fold<FT><<<s->fold_grid, 256, 0, st>>>(a);
         k_finalize<FT><<<1, FIN_NT, 0, st>>>(a, fused ? nparts_sw : nparts);
         if (fused) {
             k_mass_partials<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a, 1);
