@@ -347,6 +347,29 @@ def run_ours(args, world, rank, local):
                                                               / max(1, pst.elementary_steps), 2),
                 "timing": "sweep-by-sweep host launches with CUDA events on the launching stream"}
 
+    # ---- the fp32-fluid / fp64-history variant on the same graph (stated tolerance 1e-6 L1)
+    fp32_leg = None
+    if not fp32 and not args.no_fp32:
+        st32 = fr.init(g, params, fluid_dtype=torch.float32)
+        sol32 = fr.Solver(g, st32, sched, params, trace_cap=16)
+        sol32.run()  # warm-up
+        _lib.check(_lib.lib.fr_init_state(n, params.damping, None, _lib.ptr(st32.fluid), 1, _lib.ptr(st32.history),
+                                          _lib.stream_ptr()))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s32 = sol32.run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t32 = reduce_max(e0.elapsed_time(e1), world) / 1000.0
+        r32 = st32.history / st32.history.sum()
+        fp32_leg = {"time_to_residual_s": t32, "edges": s32.elementary_steps, "sweeps": s32.sweeps,
+                    "edges_per_s": reduce_sum(float(s32.elementary_steps), world) / t32,
+                    "rank_l1_vs_fp64": float((r32 - rank_out).abs().sum()), "stated_tolerance": 1e-6}
+        sol32.close()
+        del st32, r32
+        torch.cuda.empty_cache()
+
     # ---- the same solve with the plain |f| score (beta = 0): more edges, more time
     plain = None
     if args.beta != 0.0 and not args.no_plain:
@@ -497,6 +520,7 @@ def run_ours(args, world, rank, local):
             "gpu_launches": launches,
             "d099": d099,
             "plain_score_schedule": plain,
+            "fp32_fluid": fp32_leg,
             "power_iteration": power,
             "ppr": ppr,
             "roofline": roofline,
@@ -534,6 +558,7 @@ def main():
     ap.add_argument("--no-d099", action="store_true", help="skip the d=0.99 solve")
     ap.add_argument("--no-ppr", action="store_true", help="skip the batched PPR (configs[3]) solve")
     ap.add_argument("--no-plain", action="store_true", help="skip the beta=0 comparison solve")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-fluid comparison solve")
     ap.add_argument("--no-power", action="store_true", help="skip the power-iteration comparison")
     args = ap.parse_args()
     world, rank, local = dist_setup()
