@@ -3,22 +3,28 @@
 // Reference semantics: engine.py:240-341 run() driving the ALGO-REF diffusion
 // step (engine.py:315-329; PAPER sec. 2.2 / 3.3) under a node-selection rule
 // (sched.py).  Because H_n + F_n = F_0 + dP H_n holds for ANY selection order
-// (PAPER Theorem 3.1), a whole frontier of nodes can diffuse at once.  One
-// sweep is:
+// (PAPER Theorem 3.1), a whole frontier of nodes can diffuse at once.
 //
-//   S  k_select      read F once (coalesced), fused exact L1 mass of F, max
-//                    score, and for every node with |f| (x weight) >= theta:
-//                    F[i] = 0, H[i] += f (swap done in registers), absorbed
-//                    mass, and a degree-binned enqueue (ballot/popc-free:
-//                    one packed block scan per tile, 3 atomics per tile)
-//   P  k_push_thread thread per node    (deg <= thread_max_degree)
-//      k_push_warp   warp per node      (128-bit coalesced column loads)
-//      k_push_block  block per hub node (adjacency staged into shared memory
-//                    by cp.async.bulk, 4-stage mbarrier pipeline)
-//                    all three: red.global.add of f*d/deg into F
-//   F  k_finalize    fixed-order reduction of the block partials (bit-
-//                    reproducible residual), counters, trace row, theta
-//                    schedule, and the loop condition for the graph.
+// Fused path (default), one sweep:
+//   k_sweep        warp per tile of 32 consecutive nodes, tiles taken in order
+//                  from segmented counters: scan F and the row offsets, select
+//                  (|f| * (deg+1)^-beta >= theta, or the other rules), take the
+//                  loaded fluid with red.add(F_i, -f) and red.add(H_i, f), then
+//                  push f*d/deg over the tile's compacted edge space (hot
+//                  targets summed in shared memory, warm targets into the
+//                  L2-resident Fw); rows with >= t2 children are queued
+//   k_push_block   block per queued hub row, adjacency streamed into shared
+//                  memory by cp.async.bulk through a 3-stage mbarrier ring
+//   k_fold         Fw back into F
+//   k_finalize     fixed-order reduction of the block partials, counters,
+//                  trace row, theta schedule, loop condition
+//   k_mass_partials / k_mass_check   (guarded) exact sum |F| before stopping
+//
+// Binned path (kernel_path = 1, the north star's literal degree bins):
+//   k_select       coalesced scan, take, block-scan enqueue into three bins
+//   k_push_thread  thread per node    (deg <= thread_max_degree)
+//   k_push_warp    warp per node      (128-bit coalesced column loads)
+//   k_push_block   block per hub node (as above), then k_fold, k_finalize
 //
 // The sweep loop is a CUDA-graph while-node: the host launches one graph per
 // solve and waits once; there is no per-sweep host round trip.
@@ -251,9 +257,6 @@ static constexpr int SW_UNROLL = FR_SW_UNROLL;
 static constexpr int DSC_TAB = 256;  // tabulated d/deg in k_sweep
 
 
-#ifndef FR_TAKE_SUB
-#define FR_TAKE_SUB 1
-#endif
 __device__ __forceinline__ double take_fluid(double *p) {
     return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
 }
@@ -262,16 +265,18 @@ __device__ __forceinline__ float take_fluid(float *p) { return atomicExch(p, 0.0
 __device__ __forceinline__ u32 warp_sum_u32(u32 v) { return __reduce_add_sync(0xffffffffu, v); }
 
 // One warp per tile of 32 consecutive nodes, one sweep per launch:
-//   * coalesced load of F and of the row offsets of the tile;
-//   * selected nodes take their fluid with an atomic exchange, so pushes of
-//     other warps that race with the selection are never lost (they are
-//     either taken now or stay in F for the next sweep: conservation is exact,
-//     PAPER Theorem 3.1 holds for any split of the fluid);
-//   * the fluid-to-history swap happens in registers (H += sent);
-//   * non-hub rows are expanded edge-per-lane over the tile's contiguous
-//     column range (dense tiles) or row by row (sparse tiles), with
-//     SW_UNROLL independent column loads in flight per lane, then
-//     red.global.add of sent*d/deg into F;
+//   * coalesced load of F and of the row offsets of the next tile into
+//     registers (and an L2 prefetch of a tile further ahead);
+//   * a selected node takes exactly the fluid value the scan loaded with a
+//     fire-and-forget red.add(F_i, -f); pushes of other warps that raced
+//     with the scan stay in F for the next sweep (conservation is exact,
+//     PAPER Theorem 3.1 holds for any split of the fluid); H_i += f likewise;
+//   * the active (non-hub) rows of the tile form one compacted edge space
+//     (warp prefix scan of their degrees); each lane takes edge p of a batch,
+//     finds its row by a 5-step shuffle binary search, and SW_UNROLL column
+//     loads per lane are in flight (two register batches, ping-ponged) ahead
+//     of the red.global.add of sent*d/deg into F (hot / warm targets to
+//     shared memory / Fw);
 //   * hub rows (deg >= t2) are queued for the block-per-node kernel.
 #ifndef FR_SW_MINB
 #define FR_SW_MINB 4
@@ -396,21 +401,13 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
         sel = sel && valid && f != (FT)0;
         const bool big = deg >= a.t2;
         const bool act = sel && !big && deg > 0;
-        // take the fluid (authoritative amount, >= f for non-negative fluid) and
-        // fetch H; both are in flight while the first column loads are issued
+        // take exactly the fluid already loaded: a fire-and-forget subtraction
+        // (fluid pushed here since the load stays in F for the next sweep), so
+        // nothing below waits on a round trip (an atomicExch + H load did)
         FT sent = (FT)0;
-        double h_old = 0.0;
         if (sel) {
-#if FR_TAKE_SUB
-            // take exactly the fluid already loaded: a fire-and-forget
-            // subtraction (fluid pushed here since the load stays in F for
-            // the next sweep), so nothing below waits on a round trip
             sent = f;
             red_add(F + i, -f);
-#else
-            sent = take_fluid(F + i);
-            h_old = a.H[i];
-#endif
         }
         // compacted edge space of the active rows of this tile
         const u32 adeg = act ? deg : 0u;
@@ -451,11 +448,7 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
         double pv = 0.0;
         if (sel) {
             const double as = fabs((double)sent);
-#if FR_TAKE_SUB
             red_add(a.H + i, (double)sent);
-#else
-            a.H[i] = h_old + (double)sent;
-#endif
             nsel++;
             if (deg == 0) {
                 absorbed += as;  // dangling: all of it leaves (PAPER sec. 3.3)
