@@ -74,6 +74,52 @@ __global__ void probe(double *F, long long n, long long window, long long per_th
     if (acc == 12345.0) *sink = acc;
 }
 
+// element-type comparison: the same target streams with f64, f32 and u64 reds
+__device__ __forceinline__ void red_t(double *p) { asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(1.0) : "memory"); }
+__device__ __forceinline__ void red_t(float *p) { asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(1.0f) : "memory"); }
+__device__ __forceinline__ void red_t(unsigned long long *p) {
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(1ull) : "memory");
+}
+template <typename T>
+__global__ void probe_type(T *F, long long n, long long window, long long per_thread, int local) {
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long nt = (long long)gridDim.x * blockDim.x;
+    for (long long k = 0; k < per_thread; k++) {
+        const long long i = k * nt + tid;
+        uint64_t h = mix((uint64_t)i * 0x9E37ull + 17);
+        long long t;
+        if (local) {
+            long long off = (long long)(h % 2001) - 1000;
+            t = ((i % n) + off + n) % n;
+        } else {
+            t = (long long)(h % (uint64_t)window);
+        }
+        red_t(F + t);
+    }
+}
+template <typename T>
+void run_type(const char *name, T *F, long long n, int blocks, int threads, long long per) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const long long nt = (long long)blocks * threads;
+    for (int local = 0; local < 2; local++) {
+        for (long long w : {1ll << 23, n}) {
+            if (local && w != n) continue;
+            probe_type<T><<<blocks, threads>>>(F, n, w, per, local);
+            cudaEventRecord(a);
+            probe_type<T><<<blocks, threads>>>(F, n, w, per, local);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            printf("%-4s %-30s %8.3f ms  %7.1f G ops/s\n", name,
+                   local ? "local +-1000, streamed" : (w == n ? "uniform, all n" : "uniform, 8M elements"), ms,
+                   per * nt / (ms * 1e6));
+        }
+    }
+}
+
 int main() {
     const long long n = 100000000;  // 800 MB of doubles
     double *F, *sink;
@@ -120,6 +166,9 @@ int main() {
             if (rep) printf("%-36s %8.3f ms  %7.1f G ops/s\n", "local, in-order dynamic chunks", ms, per * nt / (ms * 1e6));
         }
     }
+    run_type<double>("f64", F, n, blocks, threads, per);
+    run_type<float>("f32", reinterpret_cast<float *>(F), n, blocks, threads, per);
+    run_type<unsigned long long>("u64", reinterpret_cast<unsigned long long *>(F), n, blocks, threads, per);
     cudaError_t e = cudaGetLastError();
     printf("status %s\n", cudaGetErrorString(e));
     return 0;
