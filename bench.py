@@ -298,7 +298,7 @@ def run_ours(args, world, rank, local):
     rows = solver.trace_rows()
     # our kernels in the timed region: init (1) + graph prologue (2) + per sweep (fused: sweep, hub,
     # fold, finalize, guarded mass pass, guarded check = 6; binned: 5) + exact residual (2) + normalize (3)
-    per_sweep = 6 if args.path == "fused" else 5
+    per_sweep = 5 if args.path == "binned" else 6
     launches = sum(1 + 2 + per_sweep * s + 2 + 3 for s in sweeps)
 
     # correctness guard for the measured run: stopping rule met, rank normalized
@@ -312,7 +312,7 @@ def run_ours(args, world, rank, local):
     pst = solver.run(profiled=True)
     kms, kl = solver.kernel_ms, solver.kernel_launches
     peak, peak_kind = load_peaks()
-    if args.path == "fused":
+    if args.path != "binned":
         narrow = L < (1 << 32) and n < (1 << 31)  # the solver's narrow row-offset copy (fr_diffuse.cu setup)
         sweep_b, hub_b = algorithmic_bytes(n, pst.sweeps, pst.diffusions, pst.elementary_steps, pst.hub_edges, fp32,
                                            narrow)
@@ -546,7 +546,7 @@ def main():
     ap.add_argument("--decay", type=float, default=0.7, help="theta decay per sweep (adaptive: nominal)")
     ap.add_argument("--edge-frac", type=float, default=0.15,
                     help="adaptive theta: target edges pushed per sweep as a fraction of m")
-    ap.add_argument("--path", default="fused", choices=("fused", "binned"))
+    ap.add_argument("--path", default="fused", choices=("fused", "binned", "owned"))
     ap.add_argument("--hot-slots", type=int, default=0, help="0 default (2048), -1 off")
     ap.add_argument("--warm-slots", type=int, default=0, help="0 default (2^21), -1 off")
     ap.add_argument("--beta", type=float, default=0.65, help="degree exponent of the sweep score")

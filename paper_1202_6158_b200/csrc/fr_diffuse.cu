@@ -69,7 +69,9 @@ struct SolveCtl {
     u64 seg_next[SW_MAX_SEGS * SEG_PAD];  // fused path: in-order tile counters, one 128 B line each
 };
 
-enum { PATH_FUSED = 0, PATH_BINNED = 1 };
+enum { PATH_FUSED = 0, PATH_BINNED = 1, PATH_OWNED = 2 };
+// the fused and owned paths share the residual bookkeeping, hub queue and graph shape
+__host__ __device__ __forceinline__ bool fused_like(int path) { return path != PATH_BINNED; }
 
 template <typename FT>
 struct SweepArgs {
@@ -102,6 +104,8 @@ struct SweepArgs {
     int path;
     int segs;    // fused path: in-order segments (<= SW_MAX_SEGS)
     u32 chunk;   // fused path: tiles per reservation
+    u32 own_ch;  // owned path: nodes per block-owned chunk (power of two)
+
     int in_graph;
     cudaGraphConditionalHandle cond;
 };
@@ -123,6 +127,8 @@ __device__ __forceinline__ u64 hmix(u64 z) {
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
 }
+
+static constexpr u32 HOT_FLAG = 0x80000000u;
 
 // ------------------------------------------------------------------ prologue
 // Exact sum |F| and max score.  guarded: only when the fused path asked for a check.
@@ -198,8 +204,6 @@ __global__ void __launch_bounds__(FIN_NT) k_mass_check(SweepArgs<FT> a, int npar
 static constexpr int HOT_SLOTS = 2048;
 static constexpr u32 WARM_SLOTS = 2u << 20;    // cap unit: up to 8x this many warm slots
 static constexpr u32 WARM_DEFAULT = 1u << 19;  // 4 MB of fp64 fluid: best on config 5 (0.5M-16M scanned)
-static constexpr u32 HOT_FLAG = 0x80000000u;
-
 template <typename FT>
 __device__ __forceinline__ void push_one(FT *__restrict__ F, FT *__restrict__ Fw, FT *hot_acc, u32 nhot, u32 t,
                                          FT v) {
@@ -515,6 +519,242 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
     }
 }
 
+// ------------------------------------------------------------------ owned-chunk sweep (kernel_path = 2)
+// Block per chunk of own_ch consecutive nodes, chunks taken in order from one
+// counter.  70% of the generator's edges land within +-1000 ids of their
+// source, so most pushes of a chunk stay inside it: those are summed in a
+// shared-memory copy of the chunk's fluid (acc) instead of red.global.add in
+// L2, and a node reached by such pushes before its own tile is scanned
+// diffuses them in the same sweep (Gauss-Seidel within the chunk; PAPER
+// Theorem 3.1 allows any order).  At the end of the chunk what is left in acc
+// goes back to F with one coalesced red.add per non-zero node.  Pushes that
+// leave the chunk, and the slotted hot/warm targets, are handled as in k_sweep.
+#ifndef FR_OWN_NT
+#define FR_OWN_NT 256
+#endif
+#ifndef FR_OWN_MINB
+#define FR_OWN_MINB 4
+#endif
+#ifndef FR_OWN_PF
+#define FR_OWN_PF 2  // L2 prefetch distance in warp rounds
+#endif
+static constexpr int OWN_NT = FR_OWN_NT;
+static constexpr int OWN_NW = OWN_NT / 32;
+
+__device__ __forceinline__ double take_shared(double *p) {
+    return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
+}
+__device__ __forceinline__ float take_shared(float *p) { return atomicExch(p, 0.0f); }
+
+template <typename FT, bool WIDE>
+__global__ void __launch_bounds__(OWN_NT, FR_OWN_MINB) k_sweep_own(SweepArgs<FT> a) {
+    using OT = typename std::conditional<WIDE, u64, u32>::type;
+    using IT = typename std::conditional<WIDE, long long, u32>::type;
+    const OT *__restrict__ offp = WIDE ? (const OT *)a.off : (const OT *)a.off32;
+    extern __shared__ __align__(16) unsigned char own_smem[];
+    FT *acc = reinterpret_cast<FT *>(own_smem);  // [own_ch]: the chunk's incoming fluid
+    FT *hot_acc = acc + a.own_ch;                // [nhot]
+    __shared__ double red_sm[OWN_NT / 32];
+    __shared__ u64 red_sm64[OWN_NT / 32];
+    __shared__ double dsc_sm[DSC_TAB];
+    __shared__ u64 chunk_sm[2];
+    __shared__ u32 tile_ctr[2];  // next unclaimed tile of the chunk (double-buffered by chunk parity)
+    constexpr u32 FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const SolveCtl *c = a.ctl;
+    const double theta = c->theta;
+    const u64 sweep = c->sweeps;
+    const double keep_frac = 1.0 - a.d;
+    double absorbed = 0.0, mx = 0.0;
+    u64 steps = 0, nsel = 0, hsteps = 0;
+    const u32 CH = a.own_ch;
+    const IT nn = (IT)a.n;
+    const u32 *__restrict__ tgt = a.tgt;
+    FT *__restrict__ F = a.F;
+    for (u32 q = threadIdx.x; q < CH; q += OWN_NT) acc[q] = (FT)0;
+    hot_clear(hot_acc, a.nhot, OWN_NT);
+    for (int q = threadIdx.x; q < DSC_TAB; q += OWN_NT) dsc_sm[q] = q ? a.d / (double)q : 0.0;
+    const u64 nchunks = ((u64)a.n + CH - 1) / CH;
+    for (u32 it = 0;; it++) {
+        if (threadIdx.x == 0) {
+            chunk_sm[it & 1] = atomicAdd(&a.ctl->seg_next[0], 1ull);
+            tile_ctr[it & 1] = OWN_NW;  // warp w starts on tile w, then claims tiles in order
+        }
+        __syncthreads();  // chunk id visible; the previous chunk's flush is complete
+        const u64 ch = chunk_sm[it & 1];
+        if (ch >= nchunks) break;
+        const IT base = (IT)(ch * CH);
+        const u32 len = (u32)((u64)a.n - (u64)base < CH ? (u64)a.n - (u64)base : CH);
+        const u32 ntl = (len + 31) >> 5;
+        FT f_cur = (FT)0;
+        OT lo_cur = 0, end_cur = 0;
+        auto load_tile = [&](u32 lt, FT &fo, OT &loo, OT &endo) {
+            const IT b = base + (IT)(lt << 5), i = b + lane;
+            const bool v = i < nn;
+            loo = offp[v ? i : nn];
+            endo = lane == 31 ? offp[b + 32 < nn ? b + 32 : nn] : (OT)0;
+            fo = v ? F[i] : (FT)0;
+        };
+        // tiles are claimed one at a time (the tiles of a chunk differ widely in
+        // edge work), so the warps reach the flush barrier together
+        u32 *ctr = &tile_ctr[it & 1];
+        u32 lt = warp;
+        if (lt < ntl) load_tile(lt, f_cur, lo_cur, end_cur);
+        while (lt < ntl) {
+            u32 lnx = 0;
+            if (lane == 0) lnx = atomicAdd(ctr, 1u);
+            lnx = __shfl_sync(FULL, lnx, 0);
+            FT f_nx = (FT)0;
+            OT lo_nx = 0, end_nx = 0;
+            if (lnx < ntl) load_tile(lnx, f_nx, lo_nx, end_nx);
+            {
+                const u32 pf = lnx + FR_OWN_PF * OWN_NW;
+                if (pf < ntl && lane < 3) {
+                    const IT j = base + (IT)(pf << 5) + (lane & 1) * 16;
+                    const void *pa = lane < 2 ? (const void *)(F + j) : (const void *)(offp + j);
+                    if (j < nn) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+                }
+            }
+            const u32 li = (lt << 5) + lane;
+            const IT i = base + (IT)li;
+            const bool valid = li < len;
+            const OT lo = lo_cur;
+            OT hi = __shfl_down_sync(FULL, lo, 1);
+            if (lane == 31) hi = end_cur;
+            const u32 deg = (u32)(hi - lo);
+            const FT fg = f_cur;
+            const FT pend = valid ? acc[li] : (FT)0;  // pushed here earlier in this chunk
+            const FT f = fg + pend;
+            const double af = fabs((double)f);
+            double score = (a.weight && valid) ? af * a.weight[i] : af;
+            if (a.beta != 0.0f) score = af * deg_weight(a.beta, deg);
+            mx = fmax(mx, score);
+            bool sel;
+            if (a.select == FR_SELECT_PER) sel = true;
+            else if (a.select == FR_SELECT_RAND)
+                sel = (double)(hmix(((u64)a.seed << 40) ^ (sweep << 32) ^ hmix((u64)i)) >> 11) * 0x1.0p-53 < a.rand_frac;
+            else sel = score >= theta;
+            sel = sel && valid && f != (FT)0;
+            const bool big = deg >= a.t2;
+            const bool act = sel && !big && deg > 0;
+            // take: the loaded global fluid by a fire-and-forget subtraction (as
+            // k_sweep), the shared-memory part by exchange (other warps of the
+            // block may be adding to it); what arrives later stays for the flush
+            FT sent = (FT)0;
+            if (sel) {
+                const FT ps = pend != (FT)0 ? take_shared(acc + li) : (FT)0;
+                if (fg != (FT)0) red_add(F + i, -fg);
+                sent = fg + ps;
+            }
+            const u32 adeg = act ? deg : 0u;
+            u32 incl = adeg;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const u32 start = incl - adeg;
+            const u32 total = __shfl_sync(FULL, incl, 31);
+            u32 tvA[SW_UNROLL], tvB[SW_UNROLL];
+            int rvA[SW_UNROLL], rvB[SW_UNROLL];
+            auto issue = [&](u32 (&tv)[SW_UNROLL], int (&rv)[SW_UNROLL], u32 c0) {
+#pragma unroll
+                for (int u = 0; u < SW_UNROLL; u++) {
+                    const u32 p0 = c0 + (u32)(u * 32 + lane);
+                    const u32 p = p0 < total ? p0 : total - 1;
+                    int r = 0;
+#pragma unroll
+                    for (int s2 = 16; s2 > 0; s2 >>= 1) {
+                        const u32 v = __shfl_sync(FULL, start, r + s2);
+                        if (v <= p) r += s2;
+                    }
+                    const OT rlo = __shfl_sync(FULL, lo, r);
+                    const u32 rs = __shfl_sync(FULL, start, r);
+                    rv[u] = p0 < total ? r : -1;
+                    tv[u] = __ldg(tgt + rlo + (p - rs));
+                }
+            };
+            if (total) issue(tvA, rvA, 0);
+            double pv = 0.0;
+            if (sel) {
+                const double as = fabs((double)sent);
+                red_add(a.H + i, (double)sent);
+                nsel++;
+                if (deg == 0) {
+                    absorbed += as;  // dangling: all of it leaves (PAPER sec. 3.3)
+                } else {
+                    absorbed += as * keep_frac;
+                    steps += deg;
+                    pv = (double)sent * (deg < DSC_TAB ? dsc_sm[deg] : a.d / (double)deg);  // engine.py:321
+                }
+            }
+            const FT pvf = (FT)pv;
+            const bool hub = sel && big;
+            const u32 hmask = __ballot_sync(FULL, hub);
+            if (hmask) {
+                u32 hb = 0;
+                const int leader = __ffs(hmask) - 1;
+                if (lane == leader) hb = atomicAdd(&a.ctl->qcount[2], (u32)__popc(hmask));
+                hb = __shfl_sync(FULL, hb, leader);
+                if (hub) {
+                    const u32 q = hb + __popc(hmask & ((1u << lane) - 1u));
+                    a.qnode[2][q] = (u32)i;
+                    a.qval[2][q] = pvf;
+                    hsteps += deg;
+                }
+            }
+            const u32 ubase = (u32)base;
+            auto scatter = [&](const u32 (&tv)[SW_UNROLL], const int (&rv)[SW_UNROLL]) {
+#pragma unroll
+                for (int u = 0; u < SW_UNROLL; u++) {
+                    const int r = rv[u];
+                    const FT v = __shfl_sync(FULL, pvf, r < 0 ? 0 : r);
+                    if (r >= 0) {
+                        const u32 t = tv[u];
+                        const u32 lt2 = t - ubase;
+                        if (!(t & HOT_FLAG) && lt2 < len) atomicAdd(acc + lt2, v);  // inside the chunk
+                        else push_one(F, a.Fw, hot_acc, a.nhot, t, v);
+                    }
+                }
+            };
+            constexpr u32 STEP = 32 * SW_UNROLL;
+            for (u32 c0 = 0; c0 < total; c0 += 2 * STEP) {
+                if (c0 + STEP < total) issue(tvB, rvB, c0 + STEP);
+                scatter(tvA, rvA);
+                if (c0 + STEP >= total) break;
+                if (c0 + 2 * STEP < total) issue(tvA, rvA, c0 + 2 * STEP);
+                scatter(tvB, rvB);
+            }
+            f_cur = f_nx;
+            lo_cur = lo_nx;
+            end_cur = end_nx;
+            lt = lnx;
+        }
+        __syncthreads();  // every push into acc of this chunk is done
+        for (u32 q = threadIdx.x; q < len; q += OWN_NT) {
+            const FT x = acc[q];
+            if (x != (FT)0) {
+                red_add(F + base + q, x);
+                acc[q] = (FT)0;
+            }
+        }
+    }
+    hot_flush(a.Fw, hot_acc, a.nhot, OWN_NT);
+    const double ba = block_sum<OWN_NT>(absorbed, red_sm);
+    const double bx = block_max<OWN_NT>(mx, red_sm);
+    const u64 bs = block_sum_u64<OWN_NT>(steps, red_sm64);
+    const u64 bn = block_sum_u64<OWN_NT>(nsel, red_sm64);
+    const u64 bh = block_sum_u64<OWN_NT>(hsteps, red_sm64);
+    if (threadIdx.x == 0) {
+        a.part_hsteps[blockIdx.x] = bh;
+        a.part_abs[blockIdx.x] = ba;
+        a.part_max[blockIdx.x] = bx;
+        a.part_steps[blockIdx.x] = bs;
+        a.part_sel[blockIdx.x] = bn;
+        a.part_mass[blockIdx.x] = 0.0;
+    }
+}
+
 // ------------------------------------------------------------------ S: select + take + enqueue
 template <typename FT>
 __global__ void __launch_bounds__(SEL_NT) k_select(SweepArgs<FT> a) {
@@ -751,7 +991,7 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
         mx = fmax(mx, a.part_max[p]);
         steps += a.part_steps[p];
         nsel += a.part_sel[p];
-        if (a.path == PATH_FUSED) hsteps += a.part_hsteps[p];
+        if (fused_like(a.path)) hsteps += a.part_hsteps[p];
     }
     mass = block_sum<FIN_NT>(mass, sm);
     ab = block_sum<FIN_NT>(ab, sm);
@@ -765,7 +1005,7 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
     // mass is exact; fused path: pushes race with the scan, so the residual is
     // carried incrementally like the reference's R (engine.py:322-325) and
     // re-derived exactly by k_mass_check before the loop may stop.
-    const double residual = a.path == PATH_FUSED ? c->residual - ab : (nsel ? mass - ab : mass);
+    const double residual = fused_like(a.path) ? c->residual - ab : (nsel ? mass - ab : mass);
     const double theta_used = c->theta;
     c->residual = residual;
     c->diffusions += nsel;
@@ -810,7 +1050,7 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
     const bool budget = (long long)c->sweeps >= a.max_sweeps ||
                         (a.max_diffusions > 0 && (long long)c->diffusions >= a.max_diffusions);
     bool done;
-    if (a.path == PATH_FUSED) {
+    if (fused_like(a.path)) {
         // converged (by the estimate) or drained: verify with an exact sum first
         const bool maybe = residual <= a.thr || (nsel == 0 && mx == 0.0);
         c->need_check = maybe ? 1u : 0u;
@@ -886,10 +1126,24 @@ using namespace fr;
 // ====================================================================== host side
 template <typename FT>
 static void *sweep_kernel(const SweepArgs<FT> &a) {
+    if (a.path == PATH_OWNED) return a.off32 ? (void *)k_sweep_own<FT, false> : (void *)k_sweep_own<FT, true>;
     return a.off32 ? (void *)k_sweep<FT, false> : (void *)k_sweep<FT, true>;
 }
 template <typename FT>
+static int sweep_threads(const SweepArgs<FT> &a) { return a.path == PATH_OWNED ? OWN_NT : SW_NT; }
+// dynamic shared memory of the sweep kernel: the owned path's chunk fluid and hot slots
+template <typename FT>
+static size_t sweep_smem(const SweepArgs<FT> &a) {
+    return a.path == PATH_OWNED ? sizeof(FT) * ((size_t)a.own_ch + (size_t)a.nhot) : 0;
+}
+template <typename FT>
 static void launch_sweep(const SweepArgs<FT> &a, int grid, cudaStream_t st) {
+    if (a.path == PATH_OWNED) {
+        const size_t sm = sweep_smem(a);
+        if (a.off32) k_sweep_own<FT, false><<<grid, OWN_NT, sm, st>>>(a);
+        else k_sweep_own<FT, true><<<grid, OWN_NT, sm, st>>>(a);
+        return;
+    }
     if (a.off32) k_sweep<FT, false><<<grid, SW_NT, 0, st>>>(a);
     else k_sweep<FT, true><<<grid, SW_NT, 0, st>>>(a);
 }
@@ -920,12 +1174,12 @@ struct fr_solver {
 
 template <typename FT>
 static int add_kernel(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, size_t ndeps, void *func,
-                      int grid, int block, void **args) {
+                      int grid, int block, void **args, size_t smem = 0) {
     cudaKernelNodeParams p = {};
     p.func = func;
     p.gridDim = dim3((unsigned)grid);
     p.blockDim = dim3((unsigned)block);
-    p.sharedMemBytes = 0;
+    p.sharedMemBytes = (unsigned)smem;
     p.kernelParams = args;
     FR_CUDA(cudaGraphAddKernelNode(node, g, deps, ndeps, &p));
     return FR_OK;
@@ -955,10 +1209,11 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
     cp.conditional.size = 1;
     FR_CUDA(cudaGraphAddNode(&n_while, s->graph, &n_pro, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    if (a.path == PATH_FUSED) {
+    if (fused_like(a.path)) {
         // sweep -> hub pushes -> finalize -> (guarded) exact mass -> (guarded) check
         cudaGraphNode_t n_sw, n_hub, n_fold, n_fin, n_m, n_chk;
-        FR_TRY(add_kernel<FT>(body, &n_sw, nullptr, 0, sweep_kernel(a), s->sweep_grid, SW_NT, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_sw, nullptr, 0, sweep_kernel(a), s->sweep_grid, sweep_threads(a), args_a,
+                              sweep_smem(a)));
         FR_TRY(add_kernel<FT>(body, &n_hub, &n_sw, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
         FR_TRY(add_kernel<FT>(body, &n_fold, &n_hub, 1, (void *)k_fold<FT>, s->fold_grid, 256, args_a));
         FR_TRY(add_kernel<FT>(body, &n_fin, &n_fold, 1, (void *)k_finalize<FT>, 1, FIN_NT, args_ans));
@@ -1105,7 +1360,7 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.select = c.select;
     a.policy = c.policy;
     a.seed = c.seed;
-    a.path = c.kernel_path == 1 ? PATH_BINNED : PATH_FUSED;
+    a.path = c.kernel_path == 1 ? PATH_BINNED : (c.kernel_path == 2 ? PATH_OWNED : PATH_FUSED);
     a.beta = (float)c.degree_exponent;
     // op2 (1/(out+1), sched.py:131-138) is the exponent 1: no weight array needed
     if (c.select == FR_SELECT_OP2 && a.weight == nullptr) a.beta = 1.0f;
@@ -1117,6 +1372,11 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
         if (a.segs < 1) a.segs = 1;
         if (a.segs > SW_MAX_SEGS) a.segs = SW_MAX_SEGS;
         if (a.chunk < 1) a.chunk = 1;
+        const char *e3 = getenv("FR_OWN_CHUNK");
+        long long ch = e3 ? atoll(e3) : 4096;
+        u32 p2 = 256;
+        while ((long long)p2 < ch && p2 < (1u << 16)) p2 <<= 1;
+        a.own_ch = p2;
     }
     // queues: a selected node lands in exactly one bin
     const long long n = s->n, m = s->m;
@@ -1146,16 +1406,19 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     // m >= 2^32 / n >= 2^31 path, which no test-sized graph would take)
     const char *fw = getenv("FR_FORCE_WIDE");
     const bool force_wide = fw && fw[0] == '1';
-    if (a.path == PATH_FUSED && !force_wide && m < (1ll << 32) && n < (1ll << 31)) {
+    if (fused_like(a.path) && !force_wide && m < (1ll << 32) && n < (1ll << 31)) {
         FR_TRY(pool_alloc((void **)&s->off32, sizeof(u32) * (size_t)(n + 1), st));
         k_narrow_offsets<<<di.sms * 8, 256, 0, st>>>(a.off, n + 1, s->off32);
         FR_CUDA(cudaGetLastError());
         a.off32 = s->off32;
     }
 
-    s->sweep_grid = occupancy_grid<FT>(sweep_kernel(a), SW_NT, di.sms);
+    // upper bound of the sweep grid (the partial arrays are sized by it); the
+    // owned path's grid depends on its shared memory, known after the slots
+    s->sweep_grid = occupancy_grid<FT>(sweep_kernel(a), sweep_threads(a), di.sms);
     const long long wtiles = ((n + 31) / 32 + SW_NT / 32 - 1) / (SW_NT / 32);
     if (s->sweep_grid > wtiles) s->sweep_grid = (int)std::max<long long>(1, wtiles);
+    if (a.path == PATH_OWNED) s->sweep_grid = di.sms * 32;
     const int P = std::max(s->sel_grid, s->sweep_grid);
     FR_TRY(pool_alloc((void **)&s->parts, sizeof(double) * 3 * (size_t)P, st));
     FR_TRY(pool_alloc((void **)&s->parts64, sizeof(u64) * 3 * (size_t)P, st));
@@ -1175,6 +1438,18 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
         FR_TRY(prepare_slots(s, a, want_hot, want_warm, st));
     }
     s->fold_grid = (int)std::max<long long>(1, std::min<long long>((long long)di.sms * 8, ((long long)a.nslots + 255) / 256));
+    if (a.path == PATH_OWNED) {
+        const size_t sm = sweep_smem(a);
+        FR_CUDA(cudaFuncSetAttribute(sweep_kernel(a), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int per = 0;
+        FR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(a), OWN_NT, sm));
+        if (per < 1) {
+            set_error("owned sweep: %zu bytes of shared memory per block do not fit", sm);
+            return FR_ERR_ARG;
+        }
+        const long long chunks = (n + a.own_ch - 1) / a.own_ch;
+        s->sweep_grid = (int)std::max<long long>(1, std::min<long long>((long long)per * di.sms, chunks));
+    }
     return build_graph<FT>(s, a);
 }
 
@@ -1296,7 +1571,7 @@ static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve
     u32 stop = 0;
     FR_CUDA(cudaMemcpyAsync(&stop, &s->ctl->stop, sizeof(u32), cudaMemcpyDeviceToHost, st));
     FR_CUDA(cudaStreamSynchronize(st));
-    const bool fused = a.path == PATH_FUSED;
+    const bool fused = fused_like(a.path);
     while (!stop) {
         // kernel classes: 0 select/sweep, 1 thread-bin push, 2 warp-bin push, 3 block-bin push, 4 finalize
         FR_CUDA(cudaEventRecord(ev[0], st));

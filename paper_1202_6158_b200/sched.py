@@ -32,6 +32,7 @@ from . import _lib
 
 KINDS = ("max", "rand", "per", "sweep", "op", "op2")
 POLICIES = ("exhaust", "geometric", "adaptive")
+KERNEL_PATHS = ("fused", "binned", "owned")  # fr_solver_config.kernel_path 0, 1, 2
 
 
 class DeviceSchedule:
@@ -56,8 +57,8 @@ class DeviceSchedule:
         self.edge_frac = float(edge_frac)
         self.thread_max_degree = int(thread_max_degree)
         self.block_min_degree = int(block_min_degree)
-        if kernel_path not in ("fused", "binned"):
-            raise ValueError(f"kernel_path must be 'fused' or 'binned', got {kernel_path!r}")
+        if kernel_path not in KERNEL_PATHS:
+            raise ValueError(f"kernel_path must be one of {KERNEL_PATHS}, got {kernel_path!r}")
         self.kernel_path = kernel_path
         self.hot_slots = int(hot_slots)
         self.warm_slots = int(warm_slots)
@@ -94,7 +95,7 @@ class DeviceSchedule:
         c.thread_max_degree = self.thread_max_degree
         c.block_min_degree = self.block_min_degree
         c.seed = self.seed & 0xFFFFFFFF
-        c.kernel_path = 0 if self.kernel_path == "fused" else 1
+        c.kernel_path = KERNEL_PATHS.index(self.kernel_path)
         c.hot_slots = self.hot_slots
         c.warm_slots = self.warm_slots
         c.degree_exponent = self.degree_exponent

@@ -26,7 +26,7 @@ def l1(a, b):
     return float(np.abs(a - b).sum())
 
 
-@pytest.mark.parametrize("path", ["fused", "binned"])
+@pytest.mark.parametrize("path", ["fused", "binned", "owned"])
 @pytest.mark.parametrize("kind", KINDS)
 def test_small_graphs_match_reference(cuda, golden_small, oracle, kind, path):
     for tag in golden_small["tags"]:
@@ -47,7 +47,7 @@ def test_small_graphs_match_reference(cuda, golden_small, oracle, kind, path):
         assert trace.rows[-1].residual <= 1e-11 * 0.15
 
 
-@pytest.mark.parametrize("path", ["fused", "binned"])
+@pytest.mark.parametrize("path", ["fused", "binned", "owned"])
 def test_config1_matches_reference(cuda, golden_configs, path):
     """BASELINE config 1: 10k uniform graph, residual < 1e-10, fp64."""
     g = graph_from(cuda, golden_configs["cfg1_off"], golden_configs["cfg1_tgt"])
@@ -80,7 +80,7 @@ def test_sweep_counters_match_parallel_oracle(cuda, oracle):
         assert abs(state.elementary_steps - ref.elementary_steps) <= 0.02 * ref.elementary_steps
 
 
-@pytest.mark.parametrize("path", ["fused", "binned"])
+@pytest.mark.parametrize("path", ["fused", "binned", "owned"])
 def test_fp32_fluid_variant(cuda, golden_configs, path):
     """fp32 fluid / fp64 history: stated tolerance 1e-6 L1 against the fp64 reference."""
     g = graph_from(cuda, golden_configs["web5k_off"], golden_configs["web5k_tgt"])
@@ -261,7 +261,7 @@ def test_host_buffer_entry_point_with_hubs(cuda, oracle):
 
 
 @pytest.mark.parametrize("beta", [0.5, 1.0])
-@pytest.mark.parametrize("path", ["fused", "binned"])
+@pytest.mark.parametrize("path", ["fused", "binned", "owned"])
 def test_degree_exponent_sweep(cuda, oracle, beta, path):
     """Degree-scaled sweep score |f|(out+1)^-beta (PAPER sec. 4.3) converges to the same rank."""
     src, dst = oracle.gen_edges(oracle.web_config(12.0), 50_000, 23)
@@ -278,7 +278,7 @@ def test_degree_exponent_sweep(cuda, oracle, beta, path):
 
 
 @pytest.mark.parametrize("damping", [0.85, 0.99])
-@pytest.mark.parametrize("path", ["fused", "binned"])
+@pytest.mark.parametrize("path", ["fused", "binned", "owned"])
 def test_adaptive_theta(cuda, oracle, damping, path):
     """Adaptive theta (edges per sweep steered to edge_frac*m) converges to the same rank,
     and its sweep/edge counts follow the oracle's restatement of the rule."""
@@ -322,3 +322,56 @@ def test_wide_index_kernel(cuda, oracle, monkeypatch, fluid):
     if not fp32:
         e1, e2 = trace.rows[-1].elementary_steps, trace2.rows[-1].elementary_steps
         assert abs(e1 - e2) <= 0.15 * e2
+
+
+@pytest.mark.parametrize("chunk", ["256", "1024", "16384"])
+@pytest.mark.parametrize("fluid", ["fp64", "fp32"])
+def test_owned_chunk_sizes(cuda, oracle, monkeypatch, chunk, fluid):
+    """Owned-chunk sweep (shared-memory sums of in-chunk pushes, Gauss-Seidel take): the rank
+    does not depend on the chunk size, i.e. on which pushes stay in shared memory and which
+    leave the chunk through F."""
+    monkeypatch.setenv("FR_OWN_CHUNK", chunk)
+    src, dst = oracle.gen_edges(oracle.web_config(12.0), 200_000, 41)
+    off, tgt, _ = oracle.csr_build(200_000, src, dst, clean=True)
+    g = graph_from(cuda, off, tgt)
+    fp32 = fluid == "fp32"
+    params = cuda.DiffusionParams(target_error=1e-8 if fp32 else 1e-10)
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65,
+                                edge_frac=0.15, kernel_path="owned")
+    state = cuda.init(g, params, fluid_dtype=torch.float32 if fp32 else torch.float64)
+    rank, trace = cuda.run(g, params, sched, state=state)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-12, "sweep").rank
+    assert l1(rank, ref) <= (1e-6 if fp32 else 1e-9)
+    assert state.residual <= params.target_error * (1 - params.damping)
+
+
+def test_owned_conservation(cuda, oracle, monkeypatch):
+    """Owned path with small chunks (many pushes leave the chunk, the rest are summed in shared
+    memory and flushed): exact conservation after a partial run (Theorem 3.1:
+    H + F = F0 + d P H), and repeated full solves on fresh states."""
+    monkeypatch.setenv("FR_OWN_CHUNK", "256")
+    src, dst = oracle.gen_edges(oracle.web_config(8.0), 100_000, 43)
+    off, tgt, _ = oracle.csr_build(100_000, src, dst, clean=True)
+    g = graph_from(cuda, off, tgt)
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65,
+                                edge_frac=0.15, kernel_path="owned")
+    params = cuda.DiffusionParams(target_error=1e-12)
+    state = cuda.init(g, params)
+    f0 = state.fluid.cpu().numpy().copy()
+    cuda.run(g, params, sched, state=state, max_sweeps=7)
+    torch.cuda.synchronize()
+    h = state.history.cpu().numpy()
+    f = state.fluid.cpu().numpy()
+    deg = np.diff(off)
+    src_e = np.repeat(np.arange(g.n), deg)
+    push = np.zeros(g.n)
+    np.add.at(push, tgt.astype(np.int64), h[src_e] / deg[src_e])
+    assert np.abs(h + f - f0 - 0.85 * push).max() <= 1e-15
+    assert state.sweeps == 7
+    params = cuda.DiffusionParams(target_error=1e-10)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-12, "sweep").rank
+    for _ in range(2):  # the second solve starts from the counters the first one left
+        state = cuda.init(g, params)
+        rank, _ = cuda.run(g, params, sched, state=state)
+        assert l1(rank, ref) <= 1e-9
+        assert state.residual <= 1e-10 * 0.15
