@@ -316,7 +316,8 @@ def run_ours(args, world, rank, local):
         narrow = L < (1 << 32) and n < (1 << 31)  # the solver's narrow row-offset copy (fr_diffuse.cu setup)
         sweep_b, hub_b = algorithmic_bytes(n, pst.sweeps, pst.diffusions, pst.elementary_steps, pst.hub_edges, fp32,
                                            narrow)
-        classes = {"k_sweep": (kms[0], kl[0], sweep_b), "k_push_block": (kms[3], kl[3], hub_b)}
+        sweep_name = "k_sweep_own" if args.path == "owned" else "k_sweep"
+        classes = {sweep_name: (kms[0], kl[0], sweep_b), "k_push_block": (kms[3], kl[3], hub_b)}
     else:
         fb = 4 if fp32 else 8
         classes = {"k_select": (kms[0], kl[0], pst.sweeps * n * fb + pst.diffusions * (fb + 16 + 16 + 4 + fb)),
@@ -546,7 +547,7 @@ def main():
     ap.add_argument("--decay", type=float, default=0.7, help="theta decay per sweep (adaptive: nominal)")
     ap.add_argument("--edge-frac", type=float, default=0.15,
                     help="adaptive theta: target edges pushed per sweep as a fraction of m")
-    ap.add_argument("--path", default="fused", choices=("fused", "binned", "owned"))
+    ap.add_argument("--path", default="owned", choices=("fused", "binned", "owned"))
     ap.add_argument("--hot-slots", type=int, default=0, help="0 default (2048), -1 off")
     ap.add_argument("--warm-slots", type=int, default=0, help="0 default (2^21), -1 off")
     ap.add_argument("--beta", type=float, default=0.65, help="degree exponent of the sweep score")

@@ -137,9 +137,13 @@ typedef struct fr_solver_config {
     int32_t block_min_degree; /* deg >= this -> block per node (0 = default 2048)       */
     uint32_t seed;            /* FR_SELECT_RAND                          */
     int32_t kernel_path;      /* 0: fused warp-tile sweep (select, take and push in one
-                                    kernel; hubs block-per-node) -- default
+                                    kernel; hubs block-per-node) -- default of a zeroed config
                                  1: binned queues (select kernel, then thread / warp /
-                                    block-per-node push kernels)                    */
+                                    block-per-node push kernels)
+                                 2: owned chunks (as 0, but a block owns a chunk of
+                                    consecutive nodes: in-chunk pushes are summed in shared
+                                    memory and diffused in the same sweep; FR_OWN_CHUNK
+                                    nodes, default 4096) -- the Python mirror's default */
     int32_t hot_slots;        /* fused path: pushes into the hot_slots highest in-degree
                                  nodes are summed per block in shared memory first
                                  (0 = default 2048, max 2048; -1 = off)             */

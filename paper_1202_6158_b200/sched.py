@@ -39,7 +39,7 @@ class DeviceSchedule:
     """A selection rule plus its theta policy; consumed by engine.run."""
 
     def __init__(self, kind, seed=0, decay=0.5, policy="exhaust", rand_frac=0.25,
-                 edge_frac=0.2, thread_max_degree=0, block_min_degree=0, kernel_path="fused", hot_slots=0,
+                 edge_frac=0.2, thread_max_degree=0, block_min_degree=0, kernel_path="owned", hot_slots=0,
                  warm_slots=0, degree_exponent=0.0):
         if kind not in KINDS:
             raise ValueError(f"unknown scheduler kind {kind!r}; expected one of {KINDS}")

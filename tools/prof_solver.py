@@ -20,7 +20,7 @@ ap.add_argument("--policy", default="adaptive")
 ap.add_argument("--edge-frac", type=float, default=0.15)
 ap.add_argument("--decay", type=float, default=0.7)
 ap.add_argument("--fluid", default="fp64")
-ap.add_argument("--path", default="fused")
+ap.add_argument("--path", default="owned")
 ap.add_argument("--hot-slots", type=int, default=0)
 ap.add_argument("--block-min", type=int, default=0)
 ap.add_argument("--beta", type=float, default=0.65)

@@ -23,6 +23,7 @@ ap.add_argument("--beta", default="0.65")
 ap.add_argument("--policy", default="geometric")
 ap.add_argument("--edge-frac", default="0.2")
 ap.add_argument("--fluid", default="fp64")
+ap.add_argument("--path", default="fused")
 args = ap.parse_args()
 
 g, _ = gen.generate(gen.web_config(args.mean), args.n, 0)
@@ -34,7 +35,8 @@ fp32 = args.fluid == "fp32"
 for damping, decay, beta, ef in itertools.product(fl, dl, bl, el):
     params = fr.DiffusionParams(damping=damping, target_error=1e-9)
     state = fr.init(g, params, fluid_dtype=torch.float32 if fp32 else torch.float64)
-    sched = fr.make_scheduler("sweep", policy=args.policy, sweep_decay=decay, degree_exponent=beta, edge_frac=ef)
+    sched = fr.make_scheduler("sweep", policy=args.policy, sweep_decay=decay, degree_exponent=beta, edge_frac=ef,
+                              kernel_path=args.path)
     solver = fr.Solver(g, state, sched, params)
     best = None
     for rep in range(2):

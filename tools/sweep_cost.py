@@ -13,10 +13,13 @@ import paper_1202_6158_b200 as fr  # noqa: E402
 from paper_1202_6158_b200 import _lib, gen  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
+path = sys.argv[2] if len(sys.argv) > 2 else "fused"
+every = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 g, _ = gen.generate(gen.web_config(16.0), n, 0)
 params = fr.DiffusionParams(target_error=1e-9)
 state = fr.init(g, params)
-sched = fr.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15)
+sched = fr.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15,
+                           kernel_path=path)
 solver = fr.Solver(g, state, sched, params, trace_cap=1 << 12)
 for rep in range(2):
     _lib.check(_lib.lib.fr_init_state(g.n, 0.85, None, _lib.ptr(state.fluid), 0, _lib.ptr(state.history),
@@ -35,5 +38,5 @@ print(f"sweeps={len(dt)} total={dt.sum():.1f} ms  fit: {coef[0]:.3f} ms/sweep + 
       f"+ {coef[2]:.5f} ms/M diffusions  (r2={1 - ((dt - pred) ** 2).sum() / ((dt - dt.mean()) ** 2).sum():.3f})")
 print(f"fixed part {coef[0] * len(dt):.1f} ms, edge part {coef[1] * de.sum() / 1e6:.1f} ms, "
       f"diffusion part {coef[2] * dd.sum() / 1e6:.1f} ms")
-for k in range(0, len(dt), max(1, len(dt) // 12)):
+for k in range(0, len(dt), every or max(1, len(dt) // 12)):
     print(f"  sweep {k:3d}: {dt[k]:.3f} ms  edges {de[k] / 1e6:8.1f} M  diffusions {dd[k] / 1e6:6.1f} M")

@@ -39,7 +39,7 @@ for k, a in sorted(agg.items(), key=lambda x: -x[1][1])[:16]:
     print(f"{k:24s} {a[0]:8d} {a[1] * 1e3:10.2f} {a[1] / tot * 100:5.1f}% {a[2] / a[0] / 1e9:10.3f} "
           f"{a[2] / a[1] / 1e9 if a[1] else 0:7.0f}")
 res = {}
-for k in ("k_sweep", "k_push_block", "k_fold"):
+for k in ("k_sweep", "k_sweep_own", "k_push_block", "k_fold"):
     if k in agg:
         a = agg[k]
         res[k] = round(a[2] / a[0])
@@ -48,5 +48,6 @@ for k in ("k_sweep", "k_push_block", "k_fold"):
         res[k + "_launches"] = a[0]
 res["source"] = desc
 res["round"] = 1
+res["kernel_path"] = sys.argv[4] if len(sys.argv) > 4 else "owned"
 json.dump(res, open(out, "w"), indent=1)
 print("wrote", out)
