@@ -105,6 +105,7 @@ struct SweepArgs {
     int segs;    // fused path: in-order segments (<= SW_MAX_SEGS)
     u32 chunk;   // fused path: tiles per reservation
     u32 own_ch;  // owned path: nodes per block-owned chunk (power of two)
+    u32 own_rev;  // owned path: odd sweeps run in descending node order
 
     int in_graph;
     cudaGraphConditionalHandle cond;
@@ -575,21 +576,27 @@ __global__ void __launch_bounds__(OWN_NT, FR_OWN_MINB) k_sweep_own(SweepArgs<FT>
     hot_clear(hot_acc, a.nhot, OWN_NT);
     for (int q = threadIdx.x; q < DSC_TAB; q += OWN_NT) dsc_sm[q] = q ? a.d / (double)q : 0.0;
     const u64 nchunks = ((u64)a.n + CH - 1) / CH;
+    const bool rev = (sweep & 1) && a.own_rev;
     for (u32 it = 0;; it++) {
         if (threadIdx.x == 0) {
             chunk_sm[it & 1] = atomicAdd(&a.ctl->seg_next[0], 1ull);
             tile_ctr[it & 1] = OWN_NW;  // warp w starts on tile w, then claims tiles in order
         }
         __syncthreads();  // chunk id visible; the previous chunk's flush is complete
-        const u64 ch = chunk_sm[it & 1];
-        if (ch >= nchunks) break;
+        const u64 ch0 = chunk_sm[it & 1];
+        if (ch0 >= nchunks) break;
+        // odd sweeps run backwards (chunks and the tiles inside them): a node then
+        // sees this sweep's pushes from the nodes behind it in the id order as well
+        // as, the sweep before, those ahead of it (symmetric Gauss-Seidel)
+        const u64 ch = rev ? nchunks - 1 - ch0 : ch0;
         const IT base = (IT)(ch * CH);
         const u32 len = (u32)((u64)a.n - (u64)base < CH ? (u64)a.n - (u64)base : CH);
         const u32 ntl = (len + 31) >> 5;
+        auto tmap = [&](u32 lt) -> u32 { return rev ? ntl - 1 - lt : lt; };
         FT f_cur = (FT)0;
         OT lo_cur = 0, end_cur = 0;
         auto load_tile = [&](u32 lt, FT &fo, OT &loo, OT &endo) {
-            const IT b = base + (IT)(lt << 5), i = b + lane;
+            const IT b = base + (IT)(tmap(lt) << 5), i = b + lane;
             const bool v = i < nn;
             loo = offp[v ? i : nn];
             endo = lane == 31 ? offp[b + 32 < nn ? b + 32 : nn] : (OT)0;
@@ -610,12 +617,12 @@ __global__ void __launch_bounds__(OWN_NT, FR_OWN_MINB) k_sweep_own(SweepArgs<FT>
             {
                 const u32 pf = lnx + FR_OWN_PF * OWN_NW;
                 if (pf < ntl && lane < 3) {
-                    const IT j = base + (IT)(pf << 5) + (lane & 1) * 16;
+                    const IT j = base + (IT)(tmap(pf) << 5) + (lane & 1) * 16;
                     const void *pa = lane < 2 ? (const void *)(F + j) : (const void *)(offp + j);
                     if (j < nn) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
                 }
             }
-            const u32 li = (lt << 5) + lane;
+            const u32 li = (tmap(lt) << 5) + lane;
             const IT i = base + (IT)li;
             const bool valid = li < len;
             const OT lo = lo_cur;
@@ -1377,6 +1384,8 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
         u32 p2 = 256;
         while ((long long)p2 < ch && p2 < (1u << 16)) p2 <<= 1;
         a.own_ch = p2;
+        const char *e4 = getenv("FR_OWN_REV");
+        a.own_rev = e4 ? (u32)(atoi(e4) != 0) : 1u;
     }
     // queues: a selected node lands in exactly one bin
     const long long n = s->n, m = s->m;
