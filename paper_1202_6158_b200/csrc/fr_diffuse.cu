@@ -539,7 +539,14 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #ifndef FR_OWN_PF
 #define FR_OWN_PF 2  // L2 prefetch distance in warp rounds
 #endif
+#ifndef FR_OWN_PF_LANES
+#define FR_OWN_PF_LANES 3  // lanes 0, 1: fluid lines, 2: offsets, 3, 4: history lines
+#endif
+#ifndef FR_OWN_UNROLL
+#define FR_OWN_UNROLL 3  // column loads in flight per lane and batch (k_sweep: FR_SW_UNROLL)
+#endif
 static constexpr int OWN_NT = FR_OWN_NT;
+static constexpr int OWN_UNROLL = FR_OWN_UNROLL;
 static constexpr int OWN_NW = OWN_NT / 32;
 
 __device__ __forceinline__ double take_shared(double *p) {
@@ -616,9 +623,11 @@ __global__ void __launch_bounds__(OWN_NT, FR_OWN_MINB) k_sweep_own(SweepArgs<FT>
             if (lnx < ntl) load_tile(lnx, f_nx, lo_nx, end_nx);
             {
                 const u32 pf = lnx + FR_OWN_PF * OWN_NW;
-                if (pf < ntl && lane < 3) {
+                if (pf < ntl && lane < FR_OWN_PF_LANES) {
                     const IT j = base + (IT)(tmap(pf) << 5) + (lane & 1) * 16;
-                    const void *pa = lane < 2 ? (const void *)(F + j) : (const void *)(offp + j);
+                    const void *pa = lane < 2 ? (const void *)(F + j)
+                                     : lane == 2 ? (const void *)(offp + j)
+                                                 : (const void *)(a.H + j);
                     if (j < nn) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
                 }
             }
@@ -662,11 +671,11 @@ __global__ void __launch_bounds__(OWN_NT, FR_OWN_MINB) k_sweep_own(SweepArgs<FT>
             }
             const u32 start = incl - adeg;
             const u32 total = __shfl_sync(FULL, incl, 31);
-            u32 tvA[SW_UNROLL], tvB[SW_UNROLL];
-            int rvA[SW_UNROLL], rvB[SW_UNROLL];
-            auto issue = [&](u32 (&tv)[SW_UNROLL], int (&rv)[SW_UNROLL], u32 c0) {
+            u32 tvA[OWN_UNROLL], tvB[OWN_UNROLL];
+            int rvA[OWN_UNROLL], rvB[OWN_UNROLL];
+            auto issue = [&](u32 (&tv)[OWN_UNROLL], int (&rv)[OWN_UNROLL], u32 c0) {
 #pragma unroll
-                for (int u = 0; u < SW_UNROLL; u++) {
+                for (int u = 0; u < OWN_UNROLL; u++) {
                     const u32 p0 = c0 + (u32)(u * 32 + lane);
                     const u32 p = p0 < total ? p0 : total - 1;
                     int r = 0;
@@ -711,9 +720,9 @@ __global__ void __launch_bounds__(OWN_NT, FR_OWN_MINB) k_sweep_own(SweepArgs<FT>
                 }
             }
             const u32 ubase = (u32)base;
-            auto scatter = [&](const u32 (&tv)[SW_UNROLL], const int (&rv)[SW_UNROLL]) {
+            auto scatter = [&](const u32 (&tv)[OWN_UNROLL], const int (&rv)[OWN_UNROLL]) {
 #pragma unroll
-                for (int u = 0; u < SW_UNROLL; u++) {
+                for (int u = 0; u < OWN_UNROLL; u++) {
                     const int r = rv[u];
                     const FT v = __shfl_sync(FULL, pvf, r < 0 ? 0 : r);
                     if (r >= 0) {
@@ -724,7 +733,7 @@ __global__ void __launch_bounds__(OWN_NT, FR_OWN_MINB) k_sweep_own(SweepArgs<FT>
                     }
                 }
             };
-            constexpr u32 STEP = 32 * SW_UNROLL;
+            constexpr u32 STEP = 32 * OWN_UNROLL;
             for (u32 c0 = 0; c0 < total; c0 += 2 * STEP) {
                 if (c0 + STEP < total) issue(tvB, rvB, c0 + STEP);
                 scatter(tvA, rvA);
