@@ -143,7 +143,7 @@ typedef struct fr_solver_config {
                                  2: owned chunks (as 0, but a block owns a chunk of
                                     consecutive nodes: in-chunk pushes are summed in shared
                                     memory and diffused in the same sweep; FR_OWN_CHUNK
-                                    nodes, default 4096) -- the Python mirror's default */
+                                    nodes, default 2048) -- the Python mirror's default */
     int32_t hot_slots;        /* fused path: pushes into the hot_slots highest in-degree
                                  nodes are summed per block in shared memory first
                                  (0 = default 2048, max 2048; -1 = off)             */

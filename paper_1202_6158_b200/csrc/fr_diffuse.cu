@@ -531,10 +531,10 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 // goes back to F with one coalesced red.add per non-zero node.  Pushes that
 // leave the chunk, and the slotted hot/warm targets, are handled as in k_sweep.
 #ifndef FR_OWN_NT
-#define FR_OWN_NT 256
+#define FR_OWN_NT 128
 #endif
 #ifndef FR_OWN_MINB
-#define FR_OWN_MINB 4
+#define FR_OWN_MINB 8
 #endif
 #ifndef FR_OWN_PF
 #define FR_OWN_PF 2  // L2 prefetch distance in warp rounds
@@ -1389,7 +1389,7 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
         if (a.segs > SW_MAX_SEGS) a.segs = SW_MAX_SEGS;
         if (a.chunk < 1) a.chunk = 1;
         const char *e3 = getenv("FR_OWN_CHUNK");
-        long long ch = e3 ? atoll(e3) : 4096;
+        long long ch = e3 ? atoll(e3) : 2048;
         u32 p2 = 256;
         while ((long long)p2 < ch && p2 < (1u << 16)) p2 <<= 1;
         a.own_ch = p2;
@@ -1451,7 +1451,10 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.nhot = 0;
     a.nslots = 0;
     if (m > 0) {
-        const int want_hot = c.hot_slots < 0 ? 0 : (c.hot_slots ? c.hot_slots : HOT_SLOTS);
+        // owned path: 1024 hot slots, so eight 128-thread blocks (chunk fluid + hot
+        // table, 24 KB each) fit one SM's shared memory
+        const int hot_default = a.path == PATH_OWNED ? HOT_SLOTS / 2 : HOT_SLOTS;
+        const int want_hot = c.hot_slots < 0 ? 0 : (c.hot_slots ? c.hot_slots : hot_default);
         const long long want_warm = c.warm_slots < 0 ? 0 : (c.warm_slots ? c.warm_slots : (long long)WARM_DEFAULT);
         FR_TRY(prepare_slots(s, a, want_hot, want_warm, st));
     }
