@@ -25,6 +25,7 @@ ap.add_argument("--policy", default="adaptive")
 ap.add_argument("--fluid", default="fp64")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--hot-slots", type=int, default=0)
+ap.add_argument("--block-min", type=int, default=0)
 ap.add_argument("variants", nargs="+")
 args = ap.parse_args()
 
@@ -39,7 +40,8 @@ for v in args.variants:
     os.environ.update(env)
     state = fr.init(g, params, fluid_dtype=torch.float32 if fp32 else torch.float64)
     sched = fr.make_scheduler("sweep", policy=args.policy, sweep_decay=args.decay, degree_exponent=args.beta,
-                              edge_frac=args.edge_frac, kernel_path=path, hot_slots=args.hot_slots)
+                              edge_frac=args.edge_frac, kernel_path=path, hot_slots=args.hot_slots,
+                              block_min_degree=args.block_min)
     solver = fr.Solver(g, state, sched, params)
     for k, o in old.items():
         if o is None:
