@@ -441,6 +441,44 @@ def run_ours(args, world, rank, local):
         sol99.close()
         del st99
 
+    # ---- the other single-solve BASELINE configs (1: N=10k uniform, 2: N=1M web,
+    # 3: N=20M web in fp64 and fp32 fluid), same schedule, graph resident
+    others = None
+    if not args.no_configs:
+        others = {}
+        for k in (1, 2, 3):
+            gk, rk = gen.baseline_graph(k, seed=args.seed)
+            pk = fr.DiffusionParams(damping=0.85, target_error=gen.CONFIGS[k]["target_error"])
+            leg = {"n": gk.n, "edges": gk.edge_count, "target_error": pk.target_error}
+            ranks = {}
+            for fl in (("fp64", "fp32") if k == 3 else ("fp64",)):
+                f32 = fl == "fp32"
+                sk = fr.init(gk, pk, fluid_dtype=torch.float32 if f32 else torch.float64)
+                solk = fr.Solver(gk, sk, sched, pk, trace_cap=16)
+                best = None
+                for _ in range(3):  # first run: graph instantiation and first touch
+                    _lib.check(_lib.lib.fr_init_state(gk.n, 0.85, None, _lib.ptr(sk.fluid), int(f32),
+                                                      _lib.ptr(sk.history), _lib.stream_ptr()))
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    stk = solk.run()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    tk = reduce_max(e0.elapsed_time(e1), world) / 1000.0
+                    best = tk if best is None else min(best, tk)
+                ranks[fl] = sk.history / sk.history.sum()
+                leg[fl] = {"time_to_residual_s": best, "sweeps": stk.sweeps, "edges": stk.elementary_steps,
+                           "edges_per_s": stk.elementary_steps / best, "final_residual": stk.residual}
+                solk.close()
+                del sk
+            if "fp32" in ranks:
+                leg["fp32"]["rank_l1_vs_fp64"] = float((ranks["fp32"] - ranks["fp64"]).abs().sum())
+                leg["fp32"]["stated_tolerance"] = 1e-6
+            others["config%d" % k] = leg
+            del gk, ranks
+            torch.cuda.empty_cache()
+
     # ---- batched personalized PageRank (BASELINE configs[3]): 1M-node web graph,
     # 64 personalization vectors x 10 seeds, every column to L1 residual 1e-9
     ppr = None
@@ -523,7 +561,7 @@ def run_ours(args, world, rank, local):
             "plain_score_schedule": plain,
             "fp32_fluid": fp32_leg,
             "power_iteration": power,
-            "ppr": ppr,
+            "ppr": ppr, "other_configs": others,
             "roofline": roofline,
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "clocks": clocks,
@@ -561,6 +599,7 @@ def main():
     ap.add_argument("--no-plain", action="store_true", help="skip the beta=0 comparison solve")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-fluid comparison solve")
     ap.add_argument("--no-power", action="store_true", help="skip the power-iteration comparison")
+    ap.add_argument("--no-configs", action="store_true", help="skip BASELINE configs 1-3")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
