@@ -5,7 +5,16 @@
 // (sched.py).  Because H_n + F_n = F_0 + dP H_n holds for ANY selection order
 // (PAPER Theorem 3.1), a whole frontier of nodes can diffuse at once.
 //
-// Fused path (default), one sweep:
+// Owned path (kernel_path = 2, the Python default), one sweep:
+//   k_sweep_own    block of 4 warps per chunk of 2048 consecutive nodes, chunks
+//                  taken in order from one counter, tiles of the chunk claimed
+//                  one at a time; per tile as k_sweep below, except that pushes
+//                  into the block's own chunk are summed in shared memory and
+//                  taken by the chunk's later tiles in the same sweep
+//                  (Gauss-Seidel), the rest flushed to F at the chunk end; odd
+//                  sweeps run backwards; then k_push_block, k_fold, k_finalize
+//
+// Fused path (kernel_path = 0), one sweep:
 //   k_sweep        warp per tile of 32 consecutive nodes, tiles taken in order
 //                  from segmented counters: scan F and the row offsets, select
 //                  (|f| * (deg+1)^-beta >= theta, or the other rules), take the
@@ -521,8 +530,9 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 }
 
 // ------------------------------------------------------------------ owned-chunk sweep (kernel_path = 2)
-// Block per chunk of own_ch consecutive nodes, chunks taken in order from one
-// counter.  70% of the generator's edges land within +-1000 ids of their
+// Block per chunk of own_ch consecutive nodes (2048 with 128 threads: fewer
+// nodes in flight per chunk make the Gauss-Seidel below stronger), chunks
+// taken in order from one counter.  70% of the generator's edges land within +-1000 ids of their
 // source, so most pushes of a chunk stay inside it: those are summed in a
 // shared-memory copy of the chunk's fluid (acc) instead of red.global.add in
 // L2, and a node reached by such pushes before its own tile is scanned
