@@ -87,14 +87,28 @@ extern "C" int fr_device_sms(void) {
     return device_info(&di) == FR_OK ? di.sms : 0;
 }
 
+// fr_diffuse.cu: solver setup on column indices that arrive in pieces (encoded in place)
+int solver_create_pieces(int64_t n, int64_t m, const int64_t *d_offsets, uint32_t *d_targets, void *d_fluid,
+                         double *d_history, const fr_solver_config *cfg, void *stream, int count,
+                         const long long *edge_end, const cudaEvent_t *ready, fr_solver **out);
+
+static constexpr int HOST_PIECES = 8;  // column-index pieces of a large host-buffer solve
+
 extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, const uint32_t *h_targets,
                                 const fr_solver_config *cfg, double *h_rank, fr_solve_stats *h_stats) {
     if (n < 1 || m < 0 || !h_offsets || (m > 0 && !h_targets) || !cfg || !h_rank) {
         set_error("fr_pagerank_host: bad arguments");
         return FR_ERR_ARG;
     }
-    cudaStream_t st;
+    // compute on st; the CSR travels on cs: offsets first, then the column
+    // indices in pieces, so the solver setup (slot classes from the first
+    // pieces, encoding of each piece as it lands) overlaps the copy
+    cudaStream_t st, cs;
     FR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    FR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    const int pieces = m >= (1ll << 26) ? HOST_PIECES : 1;
+    cudaEvent_t ev_alloc = nullptr, ev_off = nullptr, ev_piece[HOST_PIECES] = {};
+    long long edge_end[HOST_PIECES];
     int rc = FR_OK;
     fr_solver *s = nullptr;
     int64_t *d_off = nullptr;
@@ -109,15 +123,58 @@ extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, 
             (rc = pool_alloc((void **)&d_h, sizeof(double) * (size_t)n, st)) != FR_OK ||
             (rc = pool_alloc(&d_f, fsz * (size_t)n, st)) != FR_OK)
             break;
-        if ((e = cudaMemcpyAsync(d_off, h_offsets, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice, st)) !=
-                cudaSuccess ||
-            (m > 0 && (e = cudaMemcpyAsync(d_tgt, h_targets, sizeof(uint32_t) * (size_t)m, cudaMemcpyHostToDevice,
-                                           st)) != cudaSuccess)) {
-            rc = cuda_fail(e, "cudaMemcpyAsync(H2D)", __FILE__, __LINE__);
+        if ((e = cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ev_off, cudaEventDisableTiming)) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaEventCreate", __FILE__, __LINE__);
             break;
         }
+        for (int k = 0; k < pieces && rc == FR_OK; k++)
+            if ((e = cudaEventCreateWithFlags(&ev_piece[k], cudaEventDisableTiming)) != cudaSuccess)
+                rc = cuda_fail(e, "cudaEventCreate", __FILE__, __LINE__);
+        if (rc != FR_OK) break;
+        // the copies may only start once the stream-ordered allocations exist
+        if ((e = cudaEventRecord(ev_alloc, st)) != cudaSuccess || (e = cudaStreamWaitEvent(cs, ev_alloc, 0)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(d_off, h_offsets, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice, cs)) !=
+                cudaSuccess ||
+            (e = cudaEventRecord(ev_off, cs)) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaMemcpyAsync(H2D offsets)", __FILE__, __LINE__);
+            break;
+        }
+        for (int k = 0; k < pieces; k++) {
+            const long long b = k ? edge_end[k - 1] : 0;
+            edge_end[k] = k + 1 == pieces ? (long long)m : ((long long)m * (k + 1) / pieces) & ~31ll;
+            if (edge_end[k] > b &&
+                (e = cudaMemcpyAsync(d_tgt + b, h_targets + b, sizeof(uint32_t) * (size_t)(edge_end[k] - b),
+                                     cudaMemcpyHostToDevice, cs)) != cudaSuccess) {
+                rc = cuda_fail(e, "cudaMemcpyAsync(H2D targets)", __FILE__, __LINE__);
+                break;
+            }
+            if ((e = cudaEventRecord(ev_piece[k], cs)) != cudaSuccess) {
+                rc = cuda_fail(e, "cudaEventRecord", __FILE__, __LINE__);
+                break;
+            }
+        }
+        if (rc != FR_OK) break;
         if ((rc = fr_init_state(n, cfg->damping, nullptr, d_f, cfg->fluid_fp32, d_h, st)) != FR_OK) break;
-        if ((rc = fr_solver_create(n, m, d_off, d_tgt, nullptr, d_f, d_h, cfg, 0, st, &s)) != FR_OK) break;
+        if ((e = cudaStreamWaitEvent(st, ev_off, 0)) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaStreamWaitEvent", __FILE__, __LINE__);
+            break;
+        }
+        if (pieces > 1) {
+            rc = solver_create_pieces(n, m, d_off, d_tgt, d_f, d_h, cfg, st, pieces, edge_end, ev_piece, &s);
+        } else {
+            if ((e = cudaStreamWaitEvent(st, ev_piece[0], 0)) != cudaSuccess) {
+                rc = cuda_fail(e, "cudaStreamWaitEvent", __FILE__, __LINE__);
+                break;
+            }
+            rc = fr_solver_create(n, m, d_off, d_tgt, nullptr, d_f, d_h, cfg, 0, st, &s);
+        }
+        if (rc != FR_OK) break;
+        // every piece has landed before the solve (setup may not have waited for all of them)
+        if ((e = cudaStreamWaitEvent(st, ev_piece[pieces - 1], 0)) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaStreamWaitEvent", __FILE__, __LINE__);
+            break;
+        }
         if ((rc = fr_solver_run(s, st, h_stats)) != FR_OK) break;
         // rank = history / |history|_1, computed in place, then one D2H copy
         if ((rc = fr_normalize(n, d_h, d_h, nullptr, st)) != FR_OK) break;
@@ -127,12 +184,19 @@ extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, 
         }
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) rc = cuda_fail(e, "sync", __FILE__, __LINE__);
     } while (0);
+    // the copy stream may still run after an error: let it drain before the frees
+    cudaStreamSynchronize(cs);
     if (s) fr_solver_destroy(s);
     pool_free(d_off, st);
     pool_free(d_tgt, st);
     pool_free(d_h, st);
     pool_free(d_f, st);
     cudaStreamSynchronize(st);
+    if (ev_alloc) cudaEventDestroy(ev_alloc);
+    if (ev_off) cudaEventDestroy(ev_off);
+    for (int k = 0; k < HOST_PIECES; k++)
+        if (ev_piece[k]) cudaEventDestroy(ev_piece[k]);
+    cudaStreamDestroy(cs);
     cudaStreamDestroy(st);
     return rc;
 }

@@ -1174,6 +1174,18 @@ static void launch_sweep(const SweepArgs<FT> &a, int grid, cudaStream_t st) {
     else k_sweep<FT, true><<<grid, SW_NT, 0, st>>>(a);
 }
 
+// Host-buffer entry point (fr_pagerank_host): the column indices arrive in
+// pieces on a copy stream; the slot classes are estimated from the first
+// pieces and every piece is encoded as soon as it has landed, so the setup
+// overlaps the host-to-device copy instead of following it.
+struct TargetPieces {
+    int count;                    // pieces; edge range of piece k: [edge_end[k-1], edge_end[k])
+    const long long *edge_end;    // ascending, edge_end[count-1] = m
+    const cudaEvent_t *ready;     // recorded on the copy stream after piece k
+    int sample_pieces;            // pieces whose columns decide the slot classes
+    bool in_place;                // encode into the caller's column array (the caller owns it)
+};
+
 struct fr_solver {
     long long n, m;
     int fp32;
@@ -1191,6 +1203,7 @@ struct fr_solver {
     u32 *slot_node;
     void *fw_buf;
     fr_solver_config cfg;
+    const TargetPieces *pieces;  // setup only (fr_pagerank_host); null: targets resident
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     // both instantiations are kept; only one is used per solver
@@ -1291,14 +1304,26 @@ static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long
     Scratch scratch(st);
     // in-degree estimate from 1 line in 8 (exact below 2^26 edges)
     const int shift = m >= (1ll << 26) ? 3 : 0;
-    const long long scale = 1ll << shift;
     u32 *cnt, *hist;
     FR_TRY(scratch.alloc(&cnt, (size_t)n));
     FR_TRY(scratch.alloc(&hist, (size_t)IND_BINS));
     FR_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u32) * (size_t)n, st));
     FR_CUDA(cudaMemsetAsync(hist, 0, sizeof(u32) * (size_t)IND_BINS, st));
     const int g = di.sms * 8;
-    k_sample_indeg<<<g, 256, 0, st>>>(a.tgt, m, shift, cnt);
+    const TargetPieces *tp = s->pieces;
+    auto piece_begin = [&](int k) -> long long { return k ? tp->edge_end[k - 1] : 0; };
+    double sampled = (double)m;  // edges whose columns were sampled
+    if (tp) {
+        for (int k = 0; k < tp->sample_pieces; k++) {
+            FR_CUDA(cudaStreamWaitEvent(st, tp->ready[k], 0));
+            k_sample_indeg<<<g, 256, 0, st>>>(a.tgt + piece_begin(k), tp->edge_end[k] - piece_begin(k), shift, cnt);
+        }
+        sampled = (double)tp->edge_end[tp->sample_pieces - 1];
+    } else {
+        k_sample_indeg<<<g, 256, 0, st>>>(a.tgt, m, shift, cnt);
+    }
+    // the estimate counts ~1 in `scale` of a node's in-edges
+    const double scale = (double)(1ll << shift) * (sampled > 0.0 ? (double)m / sampled : 1.0);
     k_indeg_hist<<<g, 256, 0, st>>>(cnt, n, hist);
     std::vector<u32> h(IND_BINS);
     FR_CUDA(cudaMemcpyAsync(h.data(), hist, sizeof(u32) * IND_BINS, cudaMemcpyDeviceToHost, st));
@@ -1308,7 +1333,7 @@ static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long
     for (int t = IND_BINS - 1; t >= 0; t--) ge[t] = ge[t + 1] + h[t];
     // smallest threshold >= floor (in-degree units) whose class fits the budget; IND_BINS if none
     auto threshold = [&](long long floor, unsigned long long budget) -> u32 {
-        long long t0 = (floor + scale - 1) / scale;
+        long long t0 = (long long)ceil((double)floor / scale);
         if (t0 < 1) t0 = 1;
         if (budget == 0 || t0 >= IND_BINS) return (u32)IND_BINS;
         for (long long t = t0; t < IND_BINS; t++)
@@ -1340,13 +1365,27 @@ static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long
     if (nwarm > (u32)want_warm) nwarm = (u32)want_warm;
     const u32 nslots = nhot + nwarm;
     if (nslots == 0) return FR_OK;
-    FR_TRY(pool_alloc((void **)&s->tgt_enc, sizeof(u32) * (size_t)m, st));
+    u32 *enc;
+    if (tp && tp->in_place) {
+        enc = const_cast<u32 *>(a.tgt);
+    } else {
+        FR_TRY(pool_alloc((void **)&s->tgt_enc, sizeof(u32) * (size_t)m, st));
+        enc = s->tgt_enc;
+    }
     FR_TRY(pool_alloc(&s->fw_buf, sizeof(FT) * (size_t)nslots, st));
     FR_CUDA(cudaMemsetAsync(s->fw_buf, 0, sizeof(FT) * (size_t)nslots, st));
-    k_encode_targets<<<g, 256, 0, st>>>(a.tgt, m, node_slot, s->tgt_enc);
+    if (tp) {
+        for (int k = 0; k < tp->count; k++) {  // later pieces: the stream waits for them to land
+            if (k >= tp->sample_pieces) FR_CUDA(cudaStreamWaitEvent(st, tp->ready[k], 0));
+            const long long b = piece_begin(k);
+            k_encode_targets<<<g, 256, 0, st>>>(a.tgt + b, tp->edge_end[k] - b, node_slot, enc + b);
+        }
+    } else {
+        k_encode_targets<<<g, 256, 0, st>>>(a.tgt, m, node_slot, enc);
+    }
     FR_CUDA(cudaGetLastError());
-    FR_CUDA(cudaStreamSynchronize(st));
-    a.tgt = s->tgt_enc;
+    if (!tp) FR_CUDA(cudaStreamSynchronize(st));  // (the scratch frees below are stream-ordered either way)
+    a.tgt = enc;
     a.slot_node = s->slot_node;
     a.Fw = reinterpret_cast<FT *>(s->fw_buf);
     a.nhot = nhot;
@@ -1484,9 +1523,29 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     return build_graph<FT>(s, a);
 }
 
+static int solver_create(int64_t n, int64_t m, const int64_t *d_offsets, const uint32_t *d_targets,
+                         const double *d_score_weight, void *d_fluid, double *d_history, const fr_solver_config *cfg,
+                         int64_t trace_cap, void *stream, const TargetPieces *pieces, fr_solver **out);
+
 extern "C" int fr_solver_create(int64_t n, int64_t m, const int64_t *d_offsets, const uint32_t *d_targets,
                                 const double *d_score_weight, void *d_fluid, double *d_history,
                                 const fr_solver_config *cfg, int64_t trace_cap, void *stream, fr_solver **out) {
+    return solver_create(n, m, d_offsets, d_targets, d_score_weight, d_fluid, d_history, cfg, trace_cap, stream,
+                         nullptr, out);
+}
+
+// fr_pagerank_host's variant (fr_capi.cu): targets arriving in pieces, encoded in place.
+int solver_create_pieces(int64_t n, int64_t m, const int64_t *d_offsets, uint32_t *d_targets, void *d_fluid,
+                         double *d_history, const fr_solver_config *cfg, void *stream, int count,
+                         const long long *edge_end, const cudaEvent_t *ready, fr_solver **out) {
+    TargetPieces tp{count, edge_end, ready, count > 1 ? count - 1 : count, true};
+    return solver_create(n, m, d_offsets, d_targets, nullptr, d_fluid, d_history, cfg, 0, stream,
+                         count > 0 ? &tp : nullptr, out);
+}
+
+static int solver_create(int64_t n, int64_t m, const int64_t *d_offsets, const uint32_t *d_targets,
+                         const double *d_score_weight, void *d_fluid, double *d_history, const fr_solver_config *cfg,
+                         int64_t trace_cap, void *stream, const TargetPieces *pieces, fr_solver **out) {
     if (!out || !cfg || n < 1 || n > 0xFFFFFFFFll || m < 0 || !d_offsets || !d_fluid || !d_history ||
         (m > 0 && !d_targets)) {
         set_error("fr_solver_create: bad arguments");
@@ -1517,6 +1576,7 @@ extern "C" int fr_solver_create(int64_t n, int64_t m, const int64_t *d_offsets, 
     s->fp32 = cfg->fluid_fp32 ? 1 : 0;
     s->trace_cap = trace_cap > 0 ? trace_cap : 0;
     s->stream = (cudaStream_t)stream;
+    s->pieces = pieces;
     int rc = FR_OK;
     do {
         if ((rc = pool_alloc((void **)&s->ctl, sizeof(SolveCtl), (cudaStream_t)stream)) != FR_OK) break;
@@ -1530,6 +1590,7 @@ extern "C" int fr_solver_create(int64_t n, int64_t m, const int64_t *d_offsets, 
                      : setup<double>(s, s->ad, d_offsets, d_targets, d_score_weight, d_fluid, d_history,
                                      (cudaStream_t)stream);
     } while (0);
+    s->pieces = nullptr;
     if (rc != FR_OK) {
         fr_solver_destroy(s);
         return rc;

@@ -45,3 +45,27 @@ def test_config3_fp32_tolerance_and_power_iteration(cuda):
     assert float((r32 - r64).abs().sum()) <= 1e-6
     x, trace = cuda.power_iterate(g, cuda.DiffusionParams(target_error=1e-10))
     assert float((x - r64).abs().sum()) <= 5e-9
+
+
+def test_config3_host_buffer_pieces(cuda):
+    """fr_pagerank_host on config 3 (180M edges >= 2^26): the column indices travel in
+    pieces, the slot classes come from the first pieces and every piece is encoded in
+    place as it lands. The rank equals the resident solve's within the fp64 bound and the
+    caller's host arrays are untouched."""
+    import ctypes
+    from paper_1202_6158_b200 import _lib, gen
+    g, _ = gen.generate(gen.web_config(10.0), 20_000_000, 3)
+    params = cuda.DiffusionParams(target_error=1e-9)
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15)
+    r_dev, _ = cuda.run(g, params, sched)
+    h_off = g.out_offsets.cpu().contiguous()
+    h_tgt = g.out_targets.cpu().contiguous()
+    tgt_before = h_tgt.clone()
+    cfg = sched.solver_config(params)
+    rank = np.empty(g.n)
+    stats = _lib.SolveStats()
+    _lib.check(_lib.lib.fr_pagerank_host(g.n, h_tgt.numel(), h_off.data_ptr(), h_tgt.data_ptr(),
+                                         ctypes.byref(cfg), rank.ctypes.data, ctypes.byref(stats)))
+    assert stats.residual <= 1e-9 * 0.15
+    assert float(np.abs(rank - r_dev.cpu().numpy()).sum()) <= 1e-9
+    assert torch.equal(h_tgt, tgt_before)
