@@ -146,7 +146,7 @@ typedef struct fr_solver_config {
                                     nodes, default 2048) -- the Python mirror's default */
     int32_t hot_slots;        /* fused path: pushes into the hot_slots highest in-degree
                                  nodes are summed per block in shared memory first
-                                 (0 = default 2048, max 2048; -1 = off)             */
+                                 (0 = default: 2048, owned path 512; max 2048; -1 = off) */
     double degree_exponent;   /* FR_SELECT_SWEEP score = |f| * (out_degree + 1)^-degree_exponent
                                  (0 = |f|, the reference sweep; 1 = the op2 weight of
                                  sched.py:131-138; PAPER sec. 4.3 ALGO-OP2)          */

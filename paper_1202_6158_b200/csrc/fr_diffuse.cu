@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #define FR_OWN_NT 128
 #endif
 #ifndef FR_OWN_MINB
-#define FR_OWN_MINB 8
+#define FR_OWN_MINB 9  // 9 blocks x 4 warps per SM: <= 56 registers (the 64-bit-index variant keeps 8)
 #endif
 #ifndef FR_OWN_PF
 #define FR_OWN_PF 2  // L2 prefetch distance in warp rounds
@@ -565,7 +565,7 @@ __device__ __forceinline__ double take_shared(double *p) {
 __device__ __forceinline__ float take_shared(float *p) { return atomicExch(p, 0.0f); }
 
 template <typename FT, bool WIDE>
-__global__ void __launch_bounds__(OWN_NT, FR_OWN_MINB) k_sweep_own(SweepArgs<FT> a) {
+__global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(SweepArgs<FT> a) {
     using OT = typename std::conditional<WIDE, u64, u32>::type;
     using IT = typename std::conditional<WIDE, long long, u32>::type;
     const OT *__restrict__ offp = WIDE ? (const OT *)a.off : (const OT *)a.off32;
@@ -1500,9 +1500,9 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.nhot = 0;
     a.nslots = 0;
     if (m > 0) {
-        // owned path: 1024 hot slots, so eight 128-thread blocks (chunk fluid + hot
-        // table, 24 KB each) fit one SM's shared memory
-        const int hot_default = a.path == PATH_OWNED ? HOT_SLOTS / 2 : HOT_SLOTS;
+        // owned path: 512 hot slots, so nine 128-thread blocks (chunk fluid + hot
+        // table, 20 KB each) fit one SM's shared memory
+        const int hot_default = a.path == PATH_OWNED ? HOT_SLOTS / 4 : HOT_SLOTS;
         const int want_hot = c.hot_slots < 0 ? 0 : (c.hot_slots ? c.hot_slots : hot_default);
         const long long want_warm = c.warm_slots < 0 ? 0 : (c.warm_slots ? c.warm_slots : (long long)WARM_DEFAULT);
         FR_TRY(prepare_slots(s, a, want_hot, want_warm, st));
