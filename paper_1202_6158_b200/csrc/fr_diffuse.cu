@@ -557,6 +557,7 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #endif
 static constexpr int OWN_NT = FR_OWN_NT;
 static constexpr int OWN_UNROLL = FR_OWN_UNROLL;
+static_assert(OWN_UNROLL * 6 <= 32, "packed row indices");
 static constexpr int OWN_NW = OWN_NT / 32;
 
 __device__ __forceinline__ double take_shared(double *p) {
@@ -584,7 +585,9 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
     const u64 sweep = c->sweeps;
     const double keep_frac = 1.0 - a.d;
     double absorbed = 0.0, mx = 0.0;
-    u64 steps = 0, nsel = 0, hsteps = 0;
+    // per-thread counters: 32-bit on the narrow path (a thread sees < 2^32 edges per sweep there)
+    using CT = typename std::conditional<WIDE, u64, u32>::type;
+    CT steps = 0, nsel = 0, hsteps = 0;
     const u32 CH = a.own_ch;
     const IT nn = (IT)a.n;
     const u32 *__restrict__ tgt = a.tgt;
@@ -681,9 +684,12 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
             }
             const u32 start = incl - adeg;
             const u32 total = __shfl_sync(FULL, incl, 31);
+            // column batches: the targets in registers, each lane's row (r + 1, 0 = past
+            // the end) packed 6 bits per batch slot into one register
             u32 tvA[OWN_UNROLL], tvB[OWN_UNROLL];
-            int rvA[OWN_UNROLL], rvB[OWN_UNROLL];
-            auto issue = [&](u32 (&tv)[OWN_UNROLL], int (&rv)[OWN_UNROLL], u32 c0) {
+            u32 rvA = 0, rvB = 0;
+            auto issue = [&](u32 (&tv)[OWN_UNROLL], u32 &rv, u32 c0) {
+                rv = 0;
 #pragma unroll
                 for (int u = 0; u < OWN_UNROLL; u++) {
                     const u32 p0 = c0 + (u32)(u * 32 + lane);
@@ -696,7 +702,7 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                     }
                     const OT rlo = __shfl_sync(FULL, lo, r);
                     const u32 rs = __shfl_sync(FULL, start, r);
-                    rv[u] = p0 < total ? r : -1;
+                    rv |= (p0 < total ? (u32)(r + 1) : 0u) << (6 * u);
                     tv[u] = __ldg(tgt + rlo + (p - rs));
                 }
             };
@@ -730,10 +736,10 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                 }
             }
             const u32 ubase = (u32)base;
-            auto scatter = [&](const u32 (&tv)[OWN_UNROLL], const int (&rv)[OWN_UNROLL]) {
+            auto scatter = [&](const u32 (&tv)[OWN_UNROLL], const u32 rv) {
 #pragma unroll
                 for (int u = 0; u < OWN_UNROLL; u++) {
-                    const int r = rv[u];
+                    const int r = (int)((rv >> (6 * u)) & 63u) - 1;
                     const FT v = __shfl_sync(FULL, pvf, r < 0 ? 0 : r);
                     if (r >= 0) {
                         const u32 t = tv[u];
@@ -768,9 +774,9 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
     hot_flush(a.Fw, hot_acc, a.nhot, OWN_NT);
     const double ba = block_sum<OWN_NT>(absorbed, red_sm);
     const double bx = block_max<OWN_NT>(mx, red_sm);
-    const u64 bs = block_sum_u64<OWN_NT>(steps, red_sm64);
-    const u64 bn = block_sum_u64<OWN_NT>(nsel, red_sm64);
-    const u64 bh = block_sum_u64<OWN_NT>(hsteps, red_sm64);
+    const u64 bs = block_sum_u64<OWN_NT>((u64)steps, red_sm64);
+    const u64 bn = block_sum_u64<OWN_NT>((u64)nsel, red_sm64);
+    const u64 bh = block_sum_u64<OWN_NT>((u64)hsteps, red_sm64);
     if (threadIdx.x == 0) {
         a.part_hsteps[blockIdx.x] = bh;
         a.part_abs[blockIdx.x] = ba;
