@@ -214,10 +214,12 @@ __global__ void __launch_bounds__(FIN_NT) k_mass_check(SweepArgs<FT> a, int npar
 static constexpr int HOT_SLOTS = 2048;
 static constexpr u32 WARM_SLOTS = 2u << 20;    // cap unit: up to 8x this many warm slots
 static constexpr u32 WARM_DEFAULT = 1u << 19;  // 4 MB of fp64 fluid: best on config 5 (0.5M-16M scanned)
+// Slots exist only when n <= 2^31 (prepare_slots), so a set HOT_FLAG bit can
+// only mean a slot when nslots != 0; without slots every target is a node id.
 template <typename FT>
 __device__ __forceinline__ void push_one(FT *__restrict__ F, FT *__restrict__ Fw, FT *hot_acc, u32 nhot, u32 t,
-                                         FT v) {
-    if (t & HOT_FLAG) {
+                                         FT v, bool slotted = true) {
+    if (slotted && (t & HOT_FLAG)) {
         const u32 sl = t & ~HOT_FLAG;
         if (sl < nhot) atomicAdd(hot_acc + sl, v);  // shared memory
         else red_add(Fw + sl, v);                  // compact, L2-resident
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
             for (int u = 0; u < SW_UNROLL; u++) {
                 const int r = rv[u];
                 const FT v = __shfl_sync(FULL, pvf, r < 0 ? 0 : r);
-                if (r >= 0) push_one(F, a.Fw, hot_acc, a.nhot, tv[u], v);
+                if (r >= 0) push_one(F, a.Fw, hot_acc, a.nhot, tv[u], v, a.nslots != 0);
             }
         };
         constexpr u32 STEP = 32 * SW_UNROLL;
@@ -588,6 +590,7 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
     // per-thread counters: 32-bit on the narrow path (a thread sees < 2^32 edges per sweep there)
     using CT = typename std::conditional<WIDE, u64, u32>::type;
     CT steps = 0, nsel = 0, hsteps = 0;
+    const bool slotted = a.nslots != 0;
     const u32 CH = a.own_ch;
     const IT nn = (IT)a.n;
     const u32 *__restrict__ tgt = a.tgt;
@@ -744,8 +747,8 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                     if (r >= 0) {
                         const u32 t = tv[u];
                         const u32 lt2 = t - ubase;
-                        if (!(t & HOT_FLAG) && lt2 < len) atomicAdd(acc + lt2, v);  // inside the chunk
-                        else push_one(F, a.Fw, hot_acc, a.nhot, t, v);
+                        if (!(slotted && (t & HOT_FLAG)) && lt2 < len) atomicAdd(acc + lt2, v);  // inside the chunk
+                        else push_one(F, a.Fw, hot_acc, a.nhot, t, v, slotted);
                     }
                 }
             };
@@ -891,7 +894,7 @@ __global__ void __launch_bounds__(256) k_push_thread(SweepArgs<FT> a) {
         const u32 node = qn[e];
         const FT v = qv[e];
         const u64 lo = a.off[node], hi = a.off[node + 1];
-        for (u64 k = lo; k < hi; k++) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + k), v);
+        for (u64 k = lo; k < hi; k++) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + k), v, a.nslots != 0);
     }
     __syncthreads();
     hot_flush(a.Fw, hot_acc, a.nhot, 256);
@@ -912,14 +915,14 @@ __global__ void __launch_bounds__(256) k_push_warp(SweepArgs<FT> a) {
         const u64 lo = a.off[node], hi = a.off[node + 1];
         const u64 a0 = min(hi, (lo + 3) & ~3ull);
         const u64 a1 = max(a0, hi & ~3ull);
-        if (lo + lane < a0) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + lo + lane), v);
-        if (a1 + lane < hi) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + a1 + lane), v);
+        if (lo + lane < a0) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + lo + lane), v, a.nslots != 0);
+        if (a1 + lane < hi) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + a1 + lane), v, a.nslots != 0);
         for (u64 q = (a0 >> 2) + lane; q < (a1 >> 2); q += 32) {
             const uint4 t = ld_stream_u4(tgt4 + q);
-            push_one(a.F, a.Fw, hot_acc, a.nhot, t.x, v);
-            push_one(a.F, a.Fw, hot_acc, a.nhot, t.y, v);
-            push_one(a.F, a.Fw, hot_acc, a.nhot, t.z, v);
-            push_one(a.F, a.Fw, hot_acc, a.nhot, t.w, v);
+            push_one(a.F, a.Fw, hot_acc, a.nhot, t.x, v, a.nslots != 0);
+            push_one(a.F, a.Fw, hot_acc, a.nhot, t.y, v, a.nslots != 0);
+            push_one(a.F, a.Fw, hot_acc, a.nhot, t.z, v, a.nslots != 0);
+            push_one(a.F, a.Fw, hot_acc, a.nhot, t.w, v, a.nslots != 0);
         }
     }
     __syncthreads();
@@ -976,8 +979,8 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
         const u64 lo = a.off[node], hi = a.off[node + 1];
         const u64 a0 = min(hi, (lo + 3) & ~3ull);
         const u64 a1 = max(a0, hi & ~3ull);
-        if (lo + threadIdx.x < a0) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + lo + threadIdx.x), v);
-        if (a1 + threadIdx.x < hi) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + a1 + threadIdx.x), v);
+        if (lo + threadIdx.x < a0) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + lo + threadIdx.x), v, a.nslots != 0);
+        if (a1 + threadIdx.x < hi) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + a1 + threadIdx.x), v, a.nslots != 0);
         const u64 body = a1 - a0;
         const u32 nch = (u32)((body + BLK_CHUNK - 1) / BLK_CHUNK);
         if (threadIdx.x == 0) {
@@ -1001,7 +1004,7 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
             const u32 len = (u32)min((u64)BLK_CHUNK, body - (u64)c * BLK_CHUNK);
             const u32 *sp = stage[s];
 #pragma unroll 4
-            for (u32 k = threadIdx.x; k < len; k += BLK_NT) push_one(a.F, a.Fw, hot_acc, a.nhot, sp[k], v);
+            for (u32 k = threadIdx.x; k < len; k += BLK_NT) push_one(a.F, a.Fw, hot_acc, a.nhot, sp[k], v, a.nslots != 0);
             __syncthreads();  // slot s is free for the next bulk load
         }
         seq += nch;
@@ -1305,6 +1308,8 @@ static int prepare_slots(fr_solver *s, SweepArgs<FT> &a, int want_hot, long long
     if (want_warm < 0) want_warm = 0;
     if (want_warm > (long long)WARM_SLOTS * 8) want_warm = (long long)WARM_SLOTS * 8;
     const long long n = s->n, m = s->m;
+    // a slotted column carries HOT_FLAG | slot, so node ids must stay below 2^31
+    if (n > (1ll << 31)) return FR_OK;
     DeviceInfo di;
     FR_TRY(device_info(&di));
     Scratch scratch(st);

@@ -69,3 +69,29 @@ def test_config3_host_buffer_pieces(cuda):
     assert stats.residual <= 1e-9 * 0.15
     assert float(np.abs(rank - r_dev.cpu().numpy()).sum()) <= 1e-9
     assert torch.equal(h_tgt, tgt_before)
+
+
+def test_node_ids_above_2_31(cuda, oracle):
+    """Maximum sizes: n = 2^31 + 64 nodes (the 64-bit-index sweep kernel; node ids with bit 31
+    set, which a slotted column would read as a slot, so no slots are made). A 64-node graph
+    lives on the top ids and every other node is dangling; by linearity the top nodes'
+    history is the oracle's 64-node history scaled by 64/n, the others' is (1-d)/n."""
+    k = 64
+    n = (1 << 31) + k
+    base = n - k
+    src, dst = oracle.gen_edges(oracle.uniform_config(10), k, 5)
+    off_s, tgt_s, _ = oracle.csr_build(k, src, dst, clean=True)
+    off = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+    off[base:] = torch.as_tensor(off_s.astype(np.int64), device="cuda")
+    tgt = torch.as_tensor((tgt_s.astype(np.uint64) + base).astype(np.uint32).view(np.int32))
+    g = cuda.SparseGraph(n, off, tgt)
+    params = cuda.DiffusionParams(target_error=1e-10)
+    state = cuda.init(g, params)
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15)
+    cuda.run(g, params, sched, state=state)
+    h = state.history
+    ref = oracle.run_seq(off_s, tgt_s, 0.85, 1e-14, "sweep").history * (k / n)
+    assert float(np.abs(h[base:].cpu().numpy() - ref).sum()) <= 2e-10
+    low = h[:base]
+    assert float((low - 0.15 / n).abs().max()) <= 1e-24
+    assert state.residual <= 1e-10 * 0.15
