@@ -534,8 +534,8 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 // ------------------------------------------------------------------ owned-chunk sweep (kernel_path = 2)
 // Block per chunk of own_ch consecutive nodes (2048 with 128 threads: fewer
 // nodes in flight per chunk make the Gauss-Seidel below stronger), chunks
-// taken in order from one counter.  70% of the generator's edges land within +-1000 ids of their
-// source, so most pushes of a chunk stay inside it: those are summed in a
+// taken in order from one counter.  70% of the generator's edges land within
+// +-1000 ids of their source, so most pushes of a chunk stay inside it: those are summed in a
 // shared-memory copy of the chunk's fluid (acc) instead of red.global.add in
 // L2, and a node reached by such pushes before its own tile is scanned
 // diffuses them in the same sweep (Gauss-Seidel within the chunk; PAPER
