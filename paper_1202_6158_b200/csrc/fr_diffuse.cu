@@ -1015,6 +1015,10 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
 
 // ------------------------------------------------------------------ F: finalize
 template <typename FT>
+__device__ bool finalize_sweep(const SweepArgs<FT> &a, double mass, double ab, double mx, u64 steps, u64 nsel,
+                               u64 hsteps);
+
+template <typename FT>
 __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts) {
     __shared__ double sm[FIN_NT / 32];
     __shared__ u64 sm64[FIN_NT / 32];
@@ -1035,6 +1039,16 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
     nsel = block_sum_u64<FIN_NT>(nsel, sm64);
     hsteps = block_sum_u64<FIN_NT>(hsteps, sm64);
     if (threadIdx.x != 0) return;
+    const bool done = finalize_sweep(a, mass, ab, mx, steps, nsel, hsteps);
+    if (a.in_graph) cudaGraphSetConditional(a.cond, done ? 0u : 1u);
+}
+
+// The bookkeeping after a sweep (one thread): residual, counters, trace row,
+// theta schedule, loop condition.  Returns whether the loop stops (the fused
+// paths may instead ask for an exact check, c->need_check).
+template <typename FT>
+__device__ bool finalize_sweep(const SweepArgs<FT> &a, double mass, double ab, double mx, u64 steps, u64 nsel,
+                               u64 hsteps) {
     SolveCtl *c = a.ctl;
     // binned path: the select pass saw F before any push of this sweep, so its
     // mass is exact; fused path: pushes race with the scan, so the residual is
@@ -1094,7 +1108,141 @@ __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts
         done = budget || residual <= a.thr || mass == 0.0;
     }
     c->stop = done ? 1u : 0u;
-    if (a.in_graph) cudaGraphSetConditional(a.cond, done ? 0u : 1u);
+    return done;
+}
+
+// ------------------------------------------------------------------ small graphs: one block, one launch
+// For n <= SMALL_N the per-sweep launches of the graph (six kernel nodes,
+// ~40 us per sweep) cost more than the sweep itself, so a single block of
+// 1024 threads runs the whole loop: prologue, sweeps (thread per node, the
+// same selection, take and push as k_sweep, F and H resident in L2), the
+// bookkeeping of k_finalize (finalize_sweep) and the exact checks, separated
+// by block barriers.  F is read with ld.global.cg: other threads' pushes land
+// in L2, and a line a thread cached in L1 would go stale.
+static constexpr int SMALL_NT = 1024;
+static constexpr long long SMALL_N = 1 << 17;
+
+template <typename FT>
+__device__ __forceinline__ FT ld_cg(const FT *p) { return __ldcg(p); }
+
+template <typename FT>
+__global__ void __launch_bounds__(SMALL_NT, 1) k_solve_small(SweepArgs<FT> a) {
+    __shared__ double sm[SMALL_NT / 32];
+    __shared__ u64 sm64[SMALL_NT / 32];
+    __shared__ double dsc_sm[DSC_TAB];
+    __shared__ double s_red[SMALL_NT / 32][2];
+    __shared__ u64 s_red64[SMALL_NT / 32][2];
+    __shared__ double s_theta;
+    __shared__ u64 s_sweep;
+    __shared__ u32 s_stop, s_check;
+    SolveCtl *c = a.ctl;
+    const long long n = a.n;
+    FT *__restrict__ F = a.F;
+    const u64 *__restrict__ off = a.off;
+    const u32 *__restrict__ tgt = a.tgt;
+    const double keep_frac = 1.0 - a.d;
+    for (int q = threadIdx.x; q < DSC_TAB; q += SMALL_NT) dsc_sm[q] = q ? a.d / (double)q : 0.0;
+    auto score_of = [&](long long i, double af) -> double {
+        double sc = a.weight ? af * a.weight[i] : af;
+        if (a.beta != 0.0f) sc = af * deg_weight(a.beta, off[i + 1] - off[i]);
+        return sc;
+    };
+    // prologue (k_mass_partials + k_prologue): exact mass, threshold = max score
+    {
+        double mass = 0.0, mx = 0.0;
+        for (long long i = threadIdx.x; i < n; i += SMALL_NT) {
+            const double af = fabs((double)ld_cg(F + i));
+            mass += af;
+            mx = fmax(mx, score_of(i, af));
+        }
+        mass = block_sum<SMALL_NT>(mass, sm);
+        mx = block_max<SMALL_NT>(mx, sm);
+        if (threadIdx.x == 0) {
+            c->theta = mx;  // sched.py:89-90
+            c->last_max = mx;
+            c->residual = mass;
+            c->mass0 = mass;
+            c->stop = (mass <= a.thr || mass == 0.0) ? 1u : 0u;
+            s_theta = mx;
+            s_sweep = c->sweeps;
+            s_stop = c->stop;
+        }
+        __syncthreads();
+    }
+    while (!s_stop) {
+        const double theta = s_theta;
+        const u64 sweep = s_sweep;
+        double absorbed = 0.0, mx = 0.0;
+        u64 steps = 0, nsel = 0;
+        for (long long i = threadIdx.x; i < n; i += SMALL_NT) {
+            const FT f = ld_cg(F + i);
+            const double af = fabs((double)f);
+            const double score = score_of(i, af);
+            mx = fmax(mx, score);
+            bool sel;
+            if (a.select == FR_SELECT_PER) sel = true;
+            else if (a.select == FR_SELECT_RAND)
+                sel = (double)(hmix(((u64)a.seed << 40) ^ (sweep << 32) ^ hmix((u64)i)) >> 11) * 0x1.0p-53 < a.rand_frac;
+            else sel = score >= theta;
+            if (!sel || f == (FT)0) continue;
+            red_add(F + i, -f);  // take exactly the loaded fluid (as k_sweep)
+            red_add(a.H + i, (double)f);
+            nsel++;
+            const u64 lo = off[i], hi = off[i + 1];
+            const u64 deg = hi - lo;
+            if (deg == 0) {
+                absorbed += af;  // dangling: all of it leaves (PAPER sec. 3.3)
+                continue;
+            }
+            absorbed += af * keep_frac;
+            steps += deg;
+            const FT v = (FT)((double)f * (deg < DSC_TAB ? dsc_sm[deg] : a.d / (double)deg));  // engine.py:321
+            for (u64 k = lo; k < hi; k++) red_add(F + __ldg(tgt + k), v);
+        }
+        // the four sweep totals in one exchange through shared memory
+        absorbed = warp_sum(absorbed);
+        mx = warp_max(mx);
+        steps = warp_sum_u64(steps);
+        nsel = warp_sum_u64(nsel);
+        if ((threadIdx.x & 31) == 0) {
+            const int w = threadIdx.x >> 5;
+            s_red[w][0] = absorbed;
+            s_red[w][1] = mx;
+            s_red64[w][0] = steps;
+            s_red64[w][1] = nsel;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            absorbed = 0.0;
+            mx = 0.0;
+            steps = nsel = 0;
+            for (int w = 0; w < SMALL_NT / 32; w++) {
+                absorbed += s_red[w][0];
+                mx = fmax(mx, s_red[w][1]);
+                steps += s_red64[w][0];
+                nsel += s_red64[w][1];
+            }
+            __threadfence();  // the sweep's reds are visible to the exact check below
+            s_stop = finalize_sweep(a, 0.0, absorbed, mx, steps, nsel, 0ull) ? 1u : 0u;
+            s_check = c->need_check;
+            s_theta = c->theta;
+            s_sweep = c->sweeps;
+        }
+        __syncthreads();
+        if (s_check) {  // k_mass_partials + k_mass_check
+            double mass = 0.0;
+            for (long long i = threadIdx.x; i < n; i += SMALL_NT) mass += fabs((double)ld_cg(F + i));
+            mass = block_sum<SMALL_NT>(mass, sm);
+            if (threadIdx.x == 0) {
+                c->residual = mass;
+                c->need_check = 0;
+                const bool done = mass <= a.thr || mass == 0.0 || c->stop;
+                c->stop = done ? 1u : 0u;
+                s_stop = c->stop;
+            }
+            __syncthreads();
+        }
+    }
 }
 
 // ------------------------------------------------------------------ hot-set preparation
@@ -1213,6 +1361,7 @@ struct fr_solver {
     void *fw_buf;
     fr_solver_config cfg;
     const TargetPieces *pieces;  // setup only (fr_pagerank_host); null: targets resident
+    int small;                   // n <= SMALL_N: the whole solve is one k_solve_small launch
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     // both instantiations are kept; only one is used per solver
@@ -1479,12 +1628,16 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     s->thread_grid = occupancy_grid<FT>((void *)k_push_thread<FT>, 256, di.sms);
     s->warp_grid = occupancy_grid<FT>((void *)k_push_warp<FT>, 256, di.sms);
     s->block_grid = occupancy_grid<FT>((void *)k_push_block<FT>, BLK_NT, di.sms);
+    {
+        const char *e = getenv("FR_SMALL");
+        s->small = fused_like(a.path) && n <= SMALL_N && !(e && e[0] == '0');
+    }
     a.off32 = nullptr;
     // FR_FORCE_WIDE=1 keeps the 64-bit kernel on small graphs (tests of the
     // m >= 2^32 / n >= 2^31 path, which no test-sized graph would take)
     const char *fw = getenv("FR_FORCE_WIDE");
     const bool force_wide = fw && fw[0] == '1';
-    if (fused_like(a.path) && !force_wide && m < (1ll << 32) && n < (1ll << 31)) {
+    if (fused_like(a.path) && !s->small && !force_wide && m < (1ll << 32) && n < (1ll << 31)) {
         FR_TRY(pool_alloc((void **)&s->off32, sizeof(u32) * (size_t)(n + 1), st));
         k_narrow_offsets<<<di.sms * 8, 256, 0, st>>>(a.off, n + 1, s->off32);
         FR_CUDA(cudaGetLastError());
@@ -1510,7 +1663,7 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     a.Fw = nullptr;
     a.nhot = 0;
     a.nslots = 0;
-    if (m > 0) {
+    if (m > 0 && !s->small) {
         // owned path: 512 hot slots, so nine 128-thread blocks (chunk fluid + hot
         // table, 20 KB each) fit one SM's shared memory
         const int hot_default = a.path == PATH_OWNED ? HOT_SLOTS / 4 : HOT_SLOTS;
@@ -1519,6 +1672,7 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
         FR_TRY(prepare_slots(s, a, want_hot, want_warm, st));
     }
     s->fold_grid = (int)std::max<long long>(1, std::min<long long>((long long)di.sms * 8, ((long long)a.nslots + 255) / 256));
+    if (s->small) return FR_OK;  // no graph: one launch per solve
     if (a.path == PATH_OWNED) {
         const size_t sm = sweep_smem(a);
         FR_CUDA(cudaFuncSetAttribute(sweep_kernel(a), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1636,7 +1790,12 @@ extern "C" int fr_solver_run(fr_solver *s, void *stream, fr_solve_stats *h_stats
     if (!s) { set_error("fr_solver_run: null solver"); return FR_ERR_ARG; }
     cudaStream_t st = (cudaStream_t)stream;
     FR_TRY(reset_ctl(s, st));
-    FR_CUDA(cudaGraphLaunch(s->exec, st));
+    if (s->small) {
+        if (s->fp32) k_solve_small<float><<<1, SMALL_NT, 0, st>>>(s->af);
+        else k_solve_small<double><<<1, SMALL_NT, 0, st>>>(s->ad);
+    } else {
+        FR_CUDA(cudaGraphLaunch(s->exec, st));
+    }
     FR_CUDA(cudaGetLastError());
     // exact sum |F| after the loop (the stopping rule of engine.py:290-293),
     // stream-ordered into the control block; one host sync for all stats
@@ -1665,6 +1824,30 @@ static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve
     a.in_graph = 0;
     int nparts = s->sel_grid, nparts_sw = s->sweep_grid;
     FR_TRY(reset_ctl(s, st));
+    if (s->small) {  // one launch: all of it is class 0
+        for (int k = 0; k < 5; k++) { ms[k] = 0.0; launches[k] = 0; }
+        cudaEvent_t e0, e1;
+        FR_CUDA(cudaEventCreate(&e0));
+        FR_CUDA(cudaEventCreate(&e1));
+        FR_CUDA(cudaEventRecord(e0, st));
+        k_solve_small<FT><<<1, SMALL_NT, 0, st>>>(a);
+        FR_CUDA(cudaEventRecord(e1, st));
+        FR_CUDA(cudaGetLastError());
+        FR_CUDA(cudaEventSynchronize(e1));
+        float t = 0.f;
+        FR_CUDA(cudaEventElapsedTime(&t, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        ms[0] = t;
+        launches[0] = 1;
+        fr_solve_stats hs;
+        FR_TRY(read_stats(s, st, &hs));
+        double exact = 0.0;
+        FR_TRY(fr_abs_sum(s->n, (void *)a.F, s->fp32, &exact, (void *)st));
+        hs.residual = exact;
+        if (h_stats) *h_stats = hs;
+        return FR_OK;
+    }
     k_mass_partials<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a, 0);
     k_prologue<FT><<<1, FIN_NT, 0, st>>>(a, nparts);
     FR_CUDA(cudaGetLastError());

@@ -262,8 +262,11 @@ def test_host_buffer_entry_point_with_hubs(cuda, oracle):
 
 @pytest.mark.parametrize("beta", [0.5, 1.0])
 @pytest.mark.parametrize("path", ["fused", "binned", "owned"])
-def test_degree_exponent_sweep(cuda, oracle, beta, path):
-    """Degree-scaled sweep score |f|(out+1)^-beta (PAPER sec. 4.3) converges to the same rank."""
+def test_degree_exponent_sweep(cuda, oracle, monkeypatch, beta, path):
+    """Degree-scaled sweep score |f|(out+1)^-beta (PAPER sec. 4.3) converges to the same rank.
+    (The multi-block sweep kernels: the single-block small-graph solve diffuses pushes within
+    the sweep and does less work than the parallel restatement, test_small_graph_single_launch.)"""
+    monkeypatch.setenv("FR_SMALL", "0")
     src, dst = oracle.gen_edges(oracle.web_config(12.0), 50_000, 23)
     off, tgt, _ = oracle.csr_build(50_000, src, dst, clean=True)
     g = graph_from(cuda, off, tgt)
@@ -279,9 +282,10 @@ def test_degree_exponent_sweep(cuda, oracle, beta, path):
 
 @pytest.mark.parametrize("damping", [0.85, 0.99])
 @pytest.mark.parametrize("path", ["fused", "binned", "owned"])
-def test_adaptive_theta(cuda, oracle, damping, path):
+def test_adaptive_theta(cuda, oracle, monkeypatch, damping, path):
     """Adaptive theta (edges per sweep steered to edge_frac*m) converges to the same rank,
-    and its sweep/edge counts follow the oracle's restatement of the rule."""
+    and its sweep/edge counts follow the oracle's restatement of the rule (multi-block kernels)."""
+    monkeypatch.setenv("FR_SMALL", "0")
     src, dst = oracle.gen_edges(oracle.web_config(12.0), 50_000, 29)
     off, tgt, _ = oracle.csr_build(50_000, src, dst, clean=True)
     g = graph_from(cuda, off, tgt)
@@ -375,3 +379,36 @@ def test_owned_conservation(cuda, oracle, monkeypatch):
         rank, _ = cuda.run(g, params, sched, state=state)
         assert l1(rank, ref) <= 1e-9
         assert state.residual <= 1e-10 * 0.15
+
+
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_small_graph_single_launch(cuda, oracle, monkeypatch, small):
+    """n <= 2^17: the whole solve runs as one single-block launch (FR_SMALL=0 forces the
+    graph of sweep kernels); both match the reference and keep conservation exact."""
+    monkeypatch.setenv("FR_SMALL", small)
+    src, dst = oracle.gen_edges(oracle.web_config(8.0), 60_000, 47)
+    off, tgt, _ = oracle.csr_build(60_000, src, dst, clean=True)
+    g = graph_from(cuda, off, tgt)
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15)
+    params = cuda.DiffusionParams(target_error=1e-12)
+    state = cuda.init(g, params)
+    f0 = state.fluid.cpu().numpy().copy()
+    cuda.run(g, params, sched, state=state, max_sweeps=5)
+    h = state.history.cpu().numpy()
+    f = state.fluid.cpu().numpy()
+    deg = np.diff(off)
+    src_e = np.repeat(np.arange(g.n), deg)
+    push = np.zeros(g.n)
+    np.add.at(push, tgt.astype(np.int64), h[src_e] / deg[src_e])
+    assert np.abs(h + f - f0 - 0.85 * push).max() <= 1e-15
+    assert state.sweeps == 5
+    params = cuda.DiffusionParams(target_error=1e-10)
+    rank, trace = cuda.run(g, params, sched)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-12, "sweep").rank
+    assert l1(rank, ref) <= 1e-9
+    assert trace.rows[-1].residual <= 1e-10 * 0.15
+    # no more work than the parallel restatement of the schedule (pushes within a sweep
+    # only let fluid merge before it moves on)
+    p = oracle.run_psweep(off, tgt, 0.85, 1e-10, policy=2, decay=0.7, weight=(deg + 1.0) ** -0.65,
+                          edge_frac=0.15)
+    assert trace.rows[-1].elementary_steps <= 1.05 * p.elementary_steps
