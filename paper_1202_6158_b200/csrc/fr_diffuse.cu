@@ -1601,6 +1601,11 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
         long long ch = e3 ? atoll(e3) : 2048;
         u32 p2 = 256;
         while ((long long)p2 < ch && p2 < (1u << 16)) p2 <<= 1;
+        // default: 2048-node chunks, halved (down to 1024) while there are fewer
+        // chunks than resident blocks (graphs below ~2.7M nodes), so every SM
+        // gets work (config 2, N=1M: 5.8 -> 5.1 ms)
+        if (!e3)
+            while (p2 > 1024 && (long long)(s->n / p2) < (long long)di.sms * FR_OWN_MINB) p2 >>= 1;
         a.own_ch = p2;
         const char *e4 = getenv("FR_OWN_REV");
         a.own_rev = e4 ? (u32)(atoi(e4) != 0) : 1u;
