@@ -23,7 +23,7 @@ h_off.copy_(g.out_offsets)
 h_tgt.copy_(g.out_targets)
 h_rank = torch.empty(n, dtype=torch.float64, pin_memory=True)
 params = fr.DiffusionParams(target_error=1e-9)
-sched = fr.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15)
+sched = fr.make_scheduler("sweep", policy="adaptive", sweep_decay=0.6, degree_exponent=0.65, edge_frac=0.2)
 cfg = sched.solver_config(params)
 
 

@@ -17,8 +17,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=100_000_000)
 ap.add_argument("--mean", type=float, default=16.0)
 ap.add_argument("--policy", default="adaptive")
-ap.add_argument("--edge-frac", type=float, default=0.15)
-ap.add_argument("--decay", type=float, default=0.7)
+ap.add_argument("--edge-frac", type=float, default=0.2)
+ap.add_argument("--decay", type=float, default=0.6)
 ap.add_argument("--fluid", default="fp64")
 ap.add_argument("--path", default="owned")
 ap.add_argument("--hot-slots", type=int, default=0)

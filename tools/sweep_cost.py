@@ -18,7 +18,7 @@ every = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 g, _ = gen.generate(gen.web_config(16.0), n, 0)
 params = fr.DiffusionParams(target_error=1e-9)
 state = fr.init(g, params)
-sched = fr.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15,
+sched = fr.make_scheduler("sweep", policy="adaptive", sweep_decay=0.6, degree_exponent=0.65, edge_frac=0.2,
                            kernel_path=path)
 solver = fr.Solver(g, state, sched, params, trace_cap=1 << 12)
 for rep in range(2):
