@@ -689,8 +689,8 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
             const u32 total = __shfl_sync(FULL, incl, 31);
             // column batches: the targets in registers, each lane's row (r + 1, 0 = past
             // the end) packed 6 bits per batch slot into one register
-            u32 tvA[OWN_UNROLL], tvB[OWN_UNROLL];
-            u32 rvA = 0, rvB = 0;
+            u32 tvA[OWN_UNROLL], tvB[OWN_UNROLL], tvC[OWN_UNROLL];
+            u32 rvA = 0, rvB = 0, rvC = 0;
             auto issue = [&](u32 (&tv)[OWN_UNROLL], u32 &rv, u32 c0) {
                 rv = 0;
 #pragma unroll
@@ -709,7 +709,10 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                     tv[u] = __ldg(tgt + rlo + (p - rs));
                 }
             };
+            constexpr u32 STEP = 32 * OWN_UNROLL;
+            // two batches in flight before the first scatter
             if (total) issue(tvA, rvA, 0);
+            if (total > STEP) issue(tvB, rvB, STEP);
             double pv = 0.0;
             if (sel) {
                 const double as = fabs((double)sent);
@@ -752,13 +755,17 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                     }
                 }
             };
-            constexpr u32 STEP = 32 * OWN_UNROLL;
-            for (u32 c0 = 0; c0 < total; c0 += 2 * STEP) {
-                if (c0 + STEP < total) issue(tvB, rvB, c0 + STEP);
+            // three rotating batches (named, so they stay in registers): two are in
+            // flight while the third is scattered
+            for (u32 c0 = 0; c0 < total; c0 += 3 * STEP) {
+                if (c0 + 2 * STEP < total) issue(tvC, rvC, c0 + 2 * STEP);
                 scatter(tvA, rvA);
                 if (c0 + STEP >= total) break;
-                if (c0 + 2 * STEP < total) issue(tvA, rvA, c0 + 2 * STEP);
+                if (c0 + 3 * STEP < total) issue(tvA, rvA, c0 + 3 * STEP);
                 scatter(tvB, rvB);
+                if (c0 + 2 * STEP >= total) break;
+                if (c0 + 4 * STEP < total) issue(tvB, rvB, c0 + 4 * STEP);
+                scatter(tvC, rvC);
             }
             f_cur = f_nx;
             lo_cur = lo_nx;
