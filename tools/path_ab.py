@@ -26,6 +26,7 @@ ap.add_argument("--fluid", default="fp64")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--hot-slots", type=int, default=0)
 ap.add_argument("--block-min", type=int, default=0)
+ap.add_argument("--warm-slots", type=int, default=0)
 ap.add_argument("variants", nargs="+")
 args = ap.parse_args()
 
@@ -41,7 +42,7 @@ for v in args.variants:
     state = fr.init(g, params, fluid_dtype=torch.float32 if fp32 else torch.float64)
     sched = fr.make_scheduler("sweep", policy=args.policy, sweep_decay=args.decay, degree_exponent=args.beta,
                               edge_frac=args.edge_frac, kernel_path=path, hot_slots=args.hot_slots,
-                              block_min_degree=args.block_min)
+                              block_min_degree=args.block_min, warm_slots=args.warm_slots)
     solver = fr.Solver(g, state, sched, params)
     for k, o in old.items():
         if o is None:
