@@ -26,9 +26,14 @@ def l1(a, b):
     return float(np.abs(a - b).sum())
 
 
-@pytest.mark.parametrize("path", ["fused", "binned", "owned"])
+@pytest.mark.parametrize("path", ["fused", "binned", "owned", "fused-graph", "owned-graph"])
 @pytest.mark.parametrize("kind", KINDS)
-def test_small_graphs_match_reference(cuda, golden_small, oracle, kind, path):
+def test_small_graphs_match_reference(cuda, golden_small, oracle, monkeypatch, kind, path):
+    """Every selection rule on the reference's small graphs; "-graph" forces the multi-block
+    sweep kernels (FR_SMALL=0) that these sizes would otherwise hand to the single-block solve."""
+    if path.endswith("-graph"):
+        monkeypatch.setenv("FR_SMALL", "0")
+        path = path[:-6]
     for tag in golden_small["tags"]:
         tag = str(tag)
         g = graph_from(cuda, golden_small[f"{tag}_off"], golden_small[f"{tag}_tgt"])
@@ -354,6 +359,7 @@ def test_owned_conservation(cuda, oracle, monkeypatch):
     memory and flushed): exact conservation after a partial run (Theorem 3.1:
     H + F = F0 + d P H), and repeated full solves on fresh states."""
     monkeypatch.setenv("FR_OWN_CHUNK", "256")
+    monkeypatch.setenv("FR_SMALL", "0")  # n = 100k would otherwise take the single-block solve
     src, dst = oracle.gen_edges(oracle.web_config(8.0), 100_000, 43)
     off, tgt, _ = oracle.csr_build(100_000, src, dst, clean=True)
     g = graph_from(cuda, off, tgt)
