@@ -1135,7 +1135,6 @@ __device__ __forceinline__ FT ld_cg(const FT *p) { return __ldcg(p); }
 template <typename FT>
 __global__ void __launch_bounds__(SMALL_NT, 1) k_solve_small(SweepArgs<FT> a) {
     __shared__ double sm[SMALL_NT / 32];
-    __shared__ u64 sm64[SMALL_NT / 32];
     __shared__ double dsc_sm[DSC_TAB];
     __shared__ double s_red[SMALL_NT / 32][2];
     __shared__ u64 s_red64[SMALL_NT / 32][2];
