@@ -47,7 +47,8 @@ def test_config3_fp32_tolerance_and_power_iteration(cuda):
     assert float((x - r64).abs().sum()) <= 5e-9
 
 
-def test_config3_host_buffer_pieces(cuda):
+@pytest.mark.parametrize("slots", ["default", "off"])
+def test_config3_host_buffer_pieces(cuda, slots):
     """fr_pagerank_host on config 3 (180M edges >= 2^26): the column indices travel in
     pieces, the slot classes come from the first pieces and every piece is encoded in
     place as it lands. The rank equals the resident solve's within the fp64 bound and the
@@ -56,7 +57,9 @@ def test_config3_host_buffer_pieces(cuda):
     from paper_1202_6158_b200 import _lib, gen
     g, _ = gen.generate(gen.web_config(10.0), 20_000_000, 3)
     params = cuda.DiffusionParams(target_error=1e-9)
-    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15)
+    kw = dict(hot_slots=-1, warm_slots=-1) if slots == "off" else {}
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15,
+                                **kw)
     r_dev, _ = cuda.run(g, params, sched)
     h_off = g.out_offsets.cpu().contiguous()
     h_tgt = g.out_targets.cpu().contiguous()
