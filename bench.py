@@ -395,7 +395,7 @@ def run_ours(args, world, rank, local):
         del st0
 
     # ---- the in-repo comparison solver on the same graph: power iteration (MAT-ITER,
-    # baseline.py:181-217) to its own stopping rule |x_n - x_{n-1}|_1 d/(1-d) <= 1e-9
+    # baseline.py:20-56) to its own stopping rule |x_n - x_{n-1}|_1 d/(1-d) <= 1e-9
     power = None
     if not args.no_power:
         t0 = time.perf_counter()
@@ -413,7 +413,7 @@ def run_ours(args, world, rank, local):
         t_pi = reduce_max(e0.elapsed_time(e1), world) / 1000.0
         power = {"time_s": t_pi, "iterations": iters, "edges": iters * L, "edges_per_s": iters * L / t_pi,
                  "transpose_build_s": t_tr, "rank_l1_vs_diffusion": float((x_pi - rank_out).abs().sum()),
-                 "stopping_rule": "|x_n - x_{n-1}|_1 * d/(1-d) <= 1e-9 (baseline.py:213)"}
+                 "stopping_rule": "|x_n - x_{n-1}|_1 * d/(1-d) <= 1e-9 (baseline.py:52)"}
         pi.close()
         del x_pi
         g._reverse = None
@@ -519,14 +519,14 @@ def run_ours(args, world, rank, local):
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     hs = _lib.SolveStats()
     # one untimed call: the first one grows the device memory pool
-    _lib.check(_lib.lib.fr_pagerank_host(n, L, h_off.data_ptr(), h_tgt.data_ptr(), ctypes.byref(cfgc),
+    _lib.check(_lib.lib.fr_pagerank_host(n, L, h_off.data_ptr(), h_tgt.data_ptr(), None, ctypes.byref(cfgc),
                                          h_rank.data_ptr(), ctypes.byref(hs)))
     e2e_edges = 0
     torch.cuda.synchronize()
     barrier(world)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        _lib.check(_lib.lib.fr_pagerank_host(n, L, h_off.data_ptr(), h_tgt.data_ptr(), ctypes.byref(cfgc),
+        _lib.check(_lib.lib.fr_pagerank_host(n, L, h_off.data_ptr(), h_tgt.data_ptr(), None, ctypes.byref(cfgc),
                                              h_rank.data_ptr(), ctypes.byref(hs)))
         e2e_edges += hs.elementary_steps
     e2e_s = time.perf_counter() - t0

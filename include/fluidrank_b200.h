@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define FR_ABI_VERSION 1
+#define FR_ABI_VERSION 2
 
 enum fr_status {
     FR_OK = 0,
@@ -99,6 +99,8 @@ int fr_diffuse_node(int64_t n, const int64_t *d_offsets, const uint32_t *d_targe
 int fr_abs_sum(int64_t n, const void *d_x, int32_t x_fp32, double *h_sum, void *stream);
 /* engine.py:235-237 _normalized: rank = history / sum|history|. */
 int fr_normalize(int64_t n, const double *d_history, double *d_rank, double *h_total, void *stream);
+/* engine.py:269-274 sample(): true error |history/|history|_1 - reference|_1. */
+int fr_l1_error(int64_t n, const double *d_history, const double *d_reference, double *h_err, void *stream);
 
 /* ------------------------------------------------------------------ */
 /* Data-parallel threshold-sweep solver: engine.py:240-341 run() with  */
@@ -198,10 +200,19 @@ int fr_solver_trace(fr_solver *s, fr_trace_row *h_rows, int64_t cap, int64_t *h_
  * time, h_launches[k] = launches. */
 int fr_solver_run_profiled(fr_solver *s, void *stream, fr_solve_stats *h_stats, double *h_ms,
                            int64_t *h_launches);
+/* engine.py:240-341 run(..., trace_every, reference): the same solve as
+ * fr_solver_run, sweeps launched from the host; after every sweep that brings
+ * the diffusion count past the next multiple of trace_every, the true L1
+ * error |h/|h|_1 - reference|_1 of that trace row is recorded (engine.py:
+ * 269-277, 334-336).  Diagnostic path (one host sync per sweep). */
+int fr_solver_run_sampled(fr_solver *s, void *stream, const double *d_reference, int64_t trace_every,
+                          fr_solve_stats *h_stats);
+/* True errors of the last sampled run, one per trace row (NaN: not sampled). */
+int fr_solver_trace_errors(fr_solver *s, double *h_err, int64_t cap, void *stream);
 int fr_solver_destroy(fr_solver *s);
 
 /* ------------------------------------------------------------------ */
-/* Power iteration (MAT-ITER): baseline.py:181-217 power_iterate on a  */
+/* Power iteration (MAT-ITER): baseline.py:20-56 power_iterate on a  */
 /* pull CSR SpMV over the transposed graph (graph.py:158-180).         */
 /* ------------------------------------------------------------------ */
 typedef struct fr_power fr_power;
@@ -237,9 +248,13 @@ int fr_ppr_normalize(int64_t n, int32_t B, const double *d_history, double *d_ra
 /* One call from host buffers (the reference-facing end-to-end path):  */
 /* H2D of the CSR, device solve, D2H of the normalized rank.           */
 /* engine.py:240-341 run(graph, params, scheduler) -> rank.            */
+/* h_teleport: n doubles, params.teleport (engine.py:56-62, 149-159);  */
+/* NULL = uniform 1/n.  Rejected like DiffusionParams.validate         */
+/* (engine.py:47-54) when negative or not summing to 1 within 1e-12.   */
 /* ------------------------------------------------------------------ */
 int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, const uint32_t *h_targets,
-                     const fr_solver_config *cfg, double *h_rank, fr_solve_stats *h_stats);
+                     const double *h_teleport, const fr_solver_config *cfg, double *h_rank,
+                     fr_solve_stats *h_stats);
 
 #ifdef __cplusplus
 }

@@ -28,7 +28,7 @@
 /* ------------------------------------------------------------------------ */
 /* numpy pairwise summation (np.sum of a contiguous float64 array).          */
 /* Used wherever the reference calls .sum(): engine.py:146 exact_residual,   */
-/* engine.py:159 init residual, engine.py:236 _normalized, baseline.py:206.  */
+/* engine.py:159 init residual, engine.py:236 _normalized, baseline.py:45.  */
 /* ------------------------------------------------------------------------ */
 static double pw_sum(const double *a, int64_t n, int absval)
 {
@@ -575,7 +575,7 @@ int fro_run_psweep(int64_t n, const int64_t *off, const uint32_t *tgt, double d,
 }
 
 /* ------------------------------------------------------------------------ */
-/* Power iteration: baseline.py:181-217.  in_off/in_src is the transposed    */
+/* Power iteration: baseline.py:20-56.  in_off/in_src is the transposed    */
 /* CSR (rows = targets, sources ascending), i.e. graph.to_matrix()'s scipy   */
 /* CSR (graph.py:158-165); the row loop is scipy's csr_matvec.              */
 /* teleport NULL = uniform 1/n.  Returns iterations, or -1 (no convergence). */

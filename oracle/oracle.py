@@ -237,7 +237,7 @@ def run_psweep(off, tgt, damping=0.85, target_error=1e-8, policy=0, decay=0.5,
 
 def power_iterate(off, tgt, damping=0.85, target_error=1e-8, teleport=None,
                   max_iterations=1_000_000, trace_every=1, trace_cap=1 << 16):
-    """baseline.py:181-217 power_iterate (scipy CSR matvec order)."""
+    """baseline.py:20-56 power_iterate (scipy CSR matvec order)."""
     n = off.size - 1
     in_off, in_src = transpose(n, off, tgt)
     out_deg = np.diff(off).astype(np.int64)

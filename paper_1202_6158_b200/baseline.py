@@ -1,8 +1,8 @@
-"""Power iteration (MAT-ITER) on the GPU: mirror of fluidrank/baseline.py:181-217.
+"""Power iteration (MAT-ITER) on the GPU: mirror of fluidrank/baseline.py:20-56.
 
 The matrix-vector product is the pull CSR SpMV of csrc/fr_spmv.cu over the
 transposed graph; the whole iteration loop runs inside one CUDA graph.
-The online ranker (OPIC, baseline.py:220-347) is not on the accelerated path.
+The online ranker (OPIC, baseline.py:59-186) is not on the accelerated path.
 """
 
 from __future__ import annotations
@@ -51,12 +51,15 @@ class PowerIteration:
             pass
 
 
-def power_iterate(graph, params, target_error=None, trace_every=1, reference=None, max_iterations=1_000_000):
+def power_iterate(graph, params, target_error=None, trace_every=1, reference=None, max_iterations=1_000_000,
+                  as_tensor=False):
     """Power iteration with dangling mass folded back through the teleport.
 
     Stops when |X_n - X_{n-1}|_1 * d/(1-d) <= target_error (params.target_error
-    by default).  Returns (rank, trace); each iteration costs L elementary
-    steps.  The loop runs on the device, so the trace holds the final row.
+    by default).  Returns (rank, trace): rank is a numpy vector like the
+    reference's (``as_tensor=True``: the device tensor); each iteration costs L
+    elementary steps.  The loop runs on the device, so the trace holds the
+    final row.
     """
     params.validate(graph.n)
     d = params.damping
@@ -75,4 +78,4 @@ def power_iterate(graph, params, target_error=None, trace_every=1, reference=Non
         ref = torch.as_tensor(reference, dtype=torch.float64).to(x.device)
         err = float((x - ref).abs().sum())
     trace.append(iters * graph.edge_count, iters, diff, diff * d / (1.0 - d), err)
-    return x, trace
+    return (x if as_tensor else x.cpu().numpy()), trace

@@ -95,10 +95,29 @@ int solver_create_pieces(int64_t n, int64_t m, const int64_t *d_offsets, uint32_
 static constexpr int HOST_PIECES = 8;  // column-index pieces of a large host-buffer solve
 
 extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, const uint32_t *h_targets,
-                                const fr_solver_config *cfg, double *h_rank, fr_solve_stats *h_stats) {
+                                const double *h_teleport, const fr_solver_config *cfg, double *h_rank,
+                                fr_solve_stats *h_stats) {
     if (n < 1 || m < 0 || !h_offsets || (m > 0 && !h_targets) || !cfg || !h_rank) {
         set_error("fr_pagerank_host: bad arguments");
         return FR_ERR_ARG;
+    }
+    if (h_teleport) {
+        // DiffusionParams.validate (engine.py:47-54): non-negative, sums to 1 within 1e-12
+        double sum = 0.0, comp = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            const double v = h_teleport[i];
+            if (!(v >= 0.0)) {
+                set_error("teleport vector has negative entries");
+                return FR_ERR_ARG;
+            }
+            const double y = v - comp, t = sum + y;  // compensated sum
+            comp = (t - sum) - y;
+            sum = t;
+        }
+        if (fabs(sum - 1.0) > 1e-12) {
+            set_error("teleport vector sums to %.17g, expected 1", sum);
+            return FR_ERR_ARG;
+        }
     }
     // compute on st; the CSR travels on cs: offsets first, then the column
     // indices in pieces, so the solver setup (slot classes from the first
@@ -107,7 +126,7 @@ extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, 
     FR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     FR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     const int pieces = m >= (1ll << 26) ? HOST_PIECES : 1;
-    cudaEvent_t ev_alloc = nullptr, ev_off = nullptr, ev_piece[HOST_PIECES] = {};
+    cudaEvent_t ev_alloc = nullptr, ev_off = nullptr, ev_tel = nullptr, ev_piece[HOST_PIECES] = {};
     long long edge_end[HOST_PIECES];
     int rc = FR_OK;
     fr_solver *s = nullptr;
@@ -124,7 +143,8 @@ extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, 
             (rc = pool_alloc(&d_f, fsz * (size_t)n, st)) != FR_OK)
             break;
         if ((e = cudaEventCreateWithFlags(&ev_alloc, cudaEventDisableTiming)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&ev_off, cudaEventDisableTiming)) != cudaSuccess) {
+            (e = cudaEventCreateWithFlags(&ev_off, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ev_tel, cudaEventDisableTiming)) != cudaSuccess) {
             rc = cuda_fail(e, "cudaEventCreate", __FILE__, __LINE__);
             break;
         }
@@ -138,6 +158,15 @@ extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, 
                 cudaSuccess ||
             (e = cudaEventRecord(ev_off, cs)) != cudaSuccess) {
             rc = cuda_fail(e, "cudaMemcpyAsync(H2D offsets)", __FILE__, __LINE__);
+            break;
+        }
+        // the teleport vector lands in the history buffer: k_init_state reads tel[i]
+        // before the same thread zeroes H[i], so no separate device copy is needed
+        if (h_teleport &&
+            ((e = cudaMemcpyAsync(d_h, h_teleport, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, cs)) !=
+                 cudaSuccess ||
+             (e = cudaEventRecord(ev_tel, cs)) != cudaSuccess)) {
+            rc = cuda_fail(e, "cudaMemcpyAsync(H2D teleport)", __FILE__, __LINE__);
             break;
         }
         for (int k = 0; k < pieces; k++) {
@@ -155,7 +184,12 @@ extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, 
             }
         }
         if (rc != FR_OK) break;
-        if ((rc = fr_init_state(n, cfg->damping, nullptr, d_f, cfg->fluid_fp32, d_h, st)) != FR_OK) break;
+        if (h_teleport && (e = cudaStreamWaitEvent(st, ev_tel, 0)) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaStreamWaitEvent", __FILE__, __LINE__);
+            break;
+        }
+        if ((rc = fr_init_state(n, cfg->damping, h_teleport ? d_h : nullptr, d_f, cfg->fluid_fp32, d_h, st)) != FR_OK)
+            break;
         if ((e = cudaStreamWaitEvent(st, ev_off, 0)) != cudaSuccess) {
             rc = cuda_fail(e, "cudaStreamWaitEvent", __FILE__, __LINE__);
             break;
@@ -194,6 +228,7 @@ extern "C" int fr_pagerank_host(int64_t n, int64_t m, const int64_t *h_offsets, 
     cudaStreamSynchronize(st);
     if (ev_alloc) cudaEventDestroy(ev_alloc);
     if (ev_off) cudaEventDestroy(ev_off);
+    if (ev_tel) cudaEventDestroy(ev_tel);
     for (int k = 0; k < HOST_PIECES; k++)
         if (ev_piece[k]) cudaEventDestroy(ev_piece[k]);
     cudaStreamDestroy(cs);

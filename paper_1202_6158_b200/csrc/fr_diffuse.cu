@@ -72,8 +72,10 @@ struct SolveCtl {
     u32 qcount[3];
     u32 stop;
     u32 need_check;     // fused path: incremental residual crossed the target, verify exactly
-    u32 pad;
+    u32 is_signed;      // the starting fluid had negative entries (an incremental-update resume)
     double exact;       // sum |F| after the run (fr_solver_run)
+    u64 next_refresh;   // signed fluid: re-derive the residual exactly once diffusions reach this
+    u64 next_trace;     // sampled runs: record the true error once diffusions reach this
     // everything above is the header copied back after a run
     u64 seg_next[SW_MAX_SEGS * SEG_PAD];  // fused path: in-order tile counters, one 128 B line each
 };
@@ -116,6 +118,12 @@ struct SweepArgs {
     u32 own_ch;  // owned path: nodes per block-owned chunk (power of two)
     u32 own_rev;  // owned path: odd sweeps run in descending node order
 
+    // sampled runs (fr_solver_run_sampled, single-block path): true L1 error of the
+    // normalized history against ref every trace_every diffusions, into true_err[row]
+    const double *ref;
+    long long trace_every;
+    double *true_err;
+
     int in_graph;
     cudaGraphConditionalHandle cond;
 };
@@ -146,38 +154,46 @@ template <typename FT>
 __global__ void __launch_bounds__(SEL_NT) k_mass_partials(SweepArgs<FT> a, int guarded) {
     __shared__ double sm[SEL_NT / 32];
     if (guarded && !a.ctl->need_check) return;
-    double mass = 0.0, mx = 0.0;
+    double mass = 0.0, mx = 0.0, neg = 0.0;
     for (long long i = blockIdx.x * (long long)SEL_NT + threadIdx.x; i < a.n; i += (long long)gridDim.x * SEL_NT) {
-        const double af = fabs((double)a.F[i]);
+        const double f = (double)a.F[i];
+        const double af = fabs(f);
         mass += af;
+        neg = fmin(neg, f);
         double score = a.weight ? af * a.weight[i] : af;
         if (a.beta != 0.0f) score = af * deg_weight(a.beta, a.off[i + 1] - a.off[i]);
         mx = fmax(mx, score);
     }
     const double bm = block_sum<SEL_NT>(mass, sm);
     const double bx = block_max<SEL_NT>(mx, sm);
+    const double bn = -block_max<SEL_NT>(-neg, sm);
     if (threadIdx.x == 0) {
         a.part_mass[blockIdx.x] = bm;
         a.part_max[blockIdx.x] = bx;
+        a.part_abs[blockIdx.x] = bn;  // most negative fluid (the prologue's signed test)
     }
 }
 
 template <typename FT>
 __global__ void __launch_bounds__(FIN_NT) k_prologue(SweepArgs<FT> a, int nparts) {
     __shared__ double sm[FIN_NT / 32];
-    double mass = 0.0, mx = 0.0;
+    double mass = 0.0, mx = 0.0, neg = 0.0;
     for (int p = threadIdx.x; p < nparts; p += FIN_NT) {
         mass += a.part_mass[p];
         mx = fmax(mx, a.part_max[p]);
+        neg = fmin(neg, a.part_abs[p]);
     }
     mass = block_sum<FIN_NT>(mass, sm);
     mx = block_max<FIN_NT>(mx, sm);
+    neg = -block_max<FIN_NT>(-neg, sm);
     if (threadIdx.x == 0) {
         SolveCtl *c = a.ctl;
         c->theta = mx;  // sched.py:89-90: threshold starts at the max fluid
         c->last_max = mx;
         c->residual = mass;
         c->mass0 = mass;
+        c->is_signed = neg < 0.0 ? 1u : 0u;
+        c->next_refresh = c->diffusions + (u64)a.n;
         c->qcount[0] = c->qcount[1] = c->qcount[2] = 0;
         for (int q = 0; q < SW_MAX_SEGS; q++) c->seg_next[q * SEG_PAD] = 0;
         c->stop = (mass <= a.thr || mass == 0.0) ? 1u : 0u;
@@ -1108,7 +1124,12 @@ __device__ bool finalize_sweep(const SweepArgs<FT> &a, double mass, double ab, d
     bool done;
     if (fused_like(a.path)) {
         // converged (by the estimate) or drained: verify with an exact sum first
-        const bool maybe = residual <= a.thr || (nsel == 0 && mx == 0.0);
+        // signed fluid: positive and negative pushes cancel, so the true |F|_1
+        // falls faster than the incremental estimate; re-derive it every n
+        // diffusions as the reference does (engine.py:331-333)
+        const bool refresh = c->is_signed && c->diffusions >= c->next_refresh;
+        if (refresh) c->next_refresh = c->diffusions + (u64)a.n;
+        const bool maybe = residual <= a.thr || (nsel == 0 && mx == 0.0) || refresh;
         c->need_check = maybe ? 1u : 0u;
         done = budget;
     } else {
@@ -1138,9 +1159,10 @@ __global__ void __launch_bounds__(SMALL_NT, 1) k_solve_small(SweepArgs<FT> a) {
     __shared__ double dsc_sm[DSC_TAB];
     __shared__ double s_red[SMALL_NT / 32][2];
     __shared__ u64 s_red64[SMALL_NT / 32][2];
-    __shared__ double s_theta;
+    __shared__ double s_theta, s_theta_h1;
     __shared__ u64 s_sweep;
-    __shared__ u32 s_stop, s_check;
+    __shared__ u32 s_stop, s_check, s_sample;
+    __shared__ u64 s_row;
     SolveCtl *c = a.ctl;
     const long long n = a.n;
     FT *__restrict__ F = a.F;
@@ -1155,19 +1177,25 @@ __global__ void __launch_bounds__(SMALL_NT, 1) k_solve_small(SweepArgs<FT> a) {
     };
     // prologue (k_mass_partials + k_prologue): exact mass, threshold = max score
     {
-        double mass = 0.0, mx = 0.0;
+        double mass = 0.0, mx = 0.0, neg = 0.0;
         for (long long i = threadIdx.x; i < n; i += SMALL_NT) {
-            const double af = fabs((double)ld_cg(F + i));
+            const double f = (double)ld_cg(F + i);
+            const double af = fabs(f);
             mass += af;
+            neg = fmin(neg, f);
             mx = fmax(mx, score_of(i, af));
         }
         mass = block_sum<SMALL_NT>(mass, sm);
         mx = block_max<SMALL_NT>(mx, sm);
+        neg = -block_max<SMALL_NT>(-neg, sm);
         if (threadIdx.x == 0) {
             c->theta = mx;  // sched.py:89-90
             c->last_max = mx;
             c->residual = mass;
             c->mass0 = mass;
+            c->is_signed = neg < 0.0 ? 1u : 0u;
+            c->next_refresh = c->diffusions + (u64)n;
+            c->next_trace = c->diffusions + (u64)a.trace_every;
             c->stop = (mass <= a.thr || mass == 0.0) ? 1u : 0u;
             s_theta = mx;
             s_sweep = c->sweeps;
@@ -1233,8 +1261,28 @@ __global__ void __launch_bounds__(SMALL_NT, 1) k_solve_small(SweepArgs<FT> a) {
             s_check = c->need_check;
             s_theta = c->theta;
             s_sweep = c->sweeps;
+            s_sample = 0;
+            if (a.ref && c->diffusions >= c->next_trace) {  // engine.py:334-336
+                s_sample = 1;
+                s_row = c->trace_len - 1;
+                c->next_trace = c->diffusions + (u64)a.trace_every;
+            }
         }
         __syncthreads();
+        if (s_sample) {  // true error of the normalized history (engine.py:269-277)
+            double h1 = 0.0;
+            for (long long i = threadIdx.x; i < n; i += SMALL_NT) h1 += fabs(ld_cg(a.H + i));
+            h1 = block_sum<SMALL_NT>(h1, sm);
+            if (threadIdx.x == 0) s_theta_h1 = h1;
+            __syncthreads();
+            const double t = s_theta_h1;
+            double e = 0.0;
+            if (t > 0.0)
+                for (long long i = threadIdx.x; i < n; i += SMALL_NT) e += fabs(ld_cg(a.H + i) / t - a.ref[i]);
+            e = block_sum<SMALL_NT>(e, sm);
+            if (threadIdx.x == 0 && t > 0.0 && (long long)s_row < a.trace_cap) a.true_err[s_row] = e;
+            __syncthreads();
+        }
         if (s_check) {  // k_mass_partials + k_mass_check
             double mass = 0.0;
             for (long long i = threadIdx.x; i < n; i += SMALL_NT) mass += fabs((double)ld_cg(F + i));
@@ -1307,6 +1355,7 @@ __global__ void k_encode_targets(const u32 *__restrict__ tgt, long long m, const
 }
 
 int abs_sum_async(long long n, const void *x, int fp32, double *d_out, cudaStream_t st);  // fr_util.cu
+int l1_error_async(long long n, const double *x, const double *ref, double *d_out, cudaStream_t st);  // fr_util.cu
 
 }  // namespace fr
 
@@ -1365,6 +1414,7 @@ struct fr_solver {
     u32 *off32;        // fused path: narrow row offsets (m < 2^32, n < 2^31), else null
     u32 *slot_node;
     void *fw_buf;
+    double *true_err;  // sampled runs: true L1 error per trace row (NaN where not sampled)
     fr_solver_config cfg;
     const TargetPieces *pieces;  // setup only (fr_pagerank_host); null: targets resident
     int small;                   // n <= SMALL_N: the whole solve is one k_solve_small launch
@@ -1916,6 +1966,94 @@ extern "C" int fr_solver_run_profiled(fr_solver *s, void *stream, fr_solve_stats
                    : run_profiled<double>(s, s->ad, st, h_stats, h_ms, h_launches);
 }
 
+// Sampled run (engine.py:240-341 with reference=...): the same sweeps as
+// fr_solver_run, launched one by one from the host (the single-block path
+// samples inside its launch); after every sweep that brings the diffusion
+// count to the next multiple of trace_every, the true L1 error of the
+// normalized history against d_reference goes into the trace row's slot.
+template <typename FT>
+static int run_sampled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, const double *ref, long long every,
+                       fr_solve_stats *h_stats) {
+    FR_TRY(reset_ctl(s, st));
+    a.ref = ref;
+    a.trace_every = every;
+    a.true_err = s->true_err;
+    a.in_graph = 0;
+    if (s->small) {
+        k_solve_small<FT><<<1, SMALL_NT, 0, st>>>(a);
+        FR_CUDA(cudaGetLastError());
+    } else {
+        const int nparts = s->sel_grid, nparts_sw = s->sweep_grid;
+        k_mass_partials<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a, 0);
+        k_prologue<FT><<<1, FIN_NT, 0, st>>>(a, nparts);
+        FR_CUDA(cudaGetLastError());
+        const bool fused = fused_like(a.path);
+        struct { u32 stop; u64 diffusions, trace_len; } h;
+        u64 next = (u64)every;
+        for (;;) {
+            FR_CUDA(cudaMemcpyAsync(&h.stop, &s->ctl->stop, sizeof(u32), cudaMemcpyDeviceToHost, st));
+            FR_CUDA(cudaMemcpyAsync(&h.diffusions, &s->ctl->diffusions, sizeof(u64), cudaMemcpyDeviceToHost, st));
+            FR_CUDA(cudaMemcpyAsync(&h.trace_len, &s->ctl->trace_len, sizeof(u64), cudaMemcpyDeviceToHost, st));
+            FR_CUDA(cudaStreamSynchronize(st));
+            if (h.trace_len > 0 && h.diffusions >= next) {
+                next = h.diffusions + (u64)every;
+                if ((long long)h.trace_len - 1 < s->trace_cap)
+                    FR_TRY(l1_error_async(s->n, a.H, ref, s->true_err + (h.trace_len - 1), st));
+            }
+            if (h.stop) break;
+            if (fused) launch_sweep<FT>(a, s->sweep_grid, st);
+            else k_select<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a);
+            if (!fused) {
+                k_push_thread<FT><<<s->thread_grid, 256, 0, st>>>(a);
+                k_push_warp<FT><<<s->warp_grid, 256, 0, st>>>(a);
+            }
+            k_push_block<FT><<<s->block_grid, BLK_NT, 0, st>>>(a);
+            k_fold<FT><<<s->fold_grid, 256, 0, st>>>(a);
+            k_finalize<FT><<<1, FIN_NT, 0, st>>>(a, fused ? nparts_sw : nparts);
+            if (fused) {
+                k_mass_partials<FT><<<s->sel_grid, SEL_NT, 0, st>>>(a, 1);
+                k_mass_check<FT><<<1, FIN_NT, 0, st>>>(a, nparts);
+            }
+            FR_CUDA(cudaGetLastError());
+        }
+    }
+    FR_TRY(abs_sum_async(s->n, (const void *)a.F, s->fp32, &s->ctl->exact, st));
+    fr_solve_stats hs;
+    double exact = 0.0;
+    FR_TRY(read_stats(s, st, &hs, &exact));
+    hs.residual = exact;
+    if (h_stats) *h_stats = hs;
+    return FR_OK;
+}
+
+extern "C" int fr_solver_run_sampled(fr_solver *s, void *stream, const double *d_reference, int64_t trace_every,
+                                     fr_solve_stats *h_stats) {
+    if (!s || !d_reference || trace_every < 1) { set_error("fr_solver_run_sampled: bad arguments"); return FR_ERR_ARG; }
+    if (s->trace_cap < 1) { set_error("fr_solver_run_sampled: the solver keeps no trace (trace_cap 0)"); return FR_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!s->true_err) FR_TRY(pool_alloc((void **)&s->true_err, sizeof(double) * (size_t)s->trace_cap, st));
+    FR_CUDA(cudaMemsetAsync(s->true_err, 0xFF, sizeof(double) * (size_t)s->trace_cap, st));  // all-ones = NaN
+    return s->fp32 ? run_sampled<float>(s, s->af, st, d_reference, trace_every, h_stats)
+                   : run_sampled<double>(s, s->ad, st, d_reference, trace_every, h_stats);
+}
+
+// True errors of the last sampled run, one per trace row (NaN: not sampled).
+extern "C" int fr_solver_trace_errors(fr_solver *s, double *h_err, int64_t cap, void *stream) {
+    if (!s || !h_err) { set_error("fr_solver_trace_errors: bad arguments"); return FR_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long k = std::min<long long>(cap, s->trace_cap);
+    if (!s->true_err) {
+        for (long long i = 0; i < cap; i++) h_err[i] = NAN;
+        return FR_OK;
+    }
+    if (k > 0) {
+        FR_CUDA(cudaMemcpyAsync(h_err, s->true_err, sizeof(double) * (size_t)k, cudaMemcpyDeviceToHost, st));
+        FR_CUDA(cudaStreamSynchronize(st));
+    }
+    for (long long i = k; i < cap; i++) h_err[i] = NAN;
+    return FR_OK;
+}
+
 extern "C" int fr_solver_trace(fr_solver *s, fr_trace_row *h_rows, int64_t cap, int64_t *h_len, void *stream) {
     if (!s) { set_error("fr_solver_trace: null solver"); return FR_ERR_ARG; }
     cudaStream_t st = (cudaStream_t)stream;
@@ -1949,6 +2087,7 @@ extern "C" int fr_solver_destroy(fr_solver *s) {
     pool_free(s->off32, st);
     pool_free(s->slot_node, st);
     pool_free(s->fw_buf, st);
+    pool_free(s->true_err, st);
     delete s;
     return FR_OK;
 }

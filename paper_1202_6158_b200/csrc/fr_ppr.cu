@@ -108,14 +108,15 @@ __global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
             double *Hi = a.H + (size_t)i * B;
             if (own0) Hi[lane] += s0;
             if (own1) Hi[lane + 32] += s1;
-            nsel++;
+            // one row visit per warp: only lane 0 counts it (the block sums add every lane)
+            if (lane == 0) nsel++;
             if (deg == 0) {
                 ab0 += fabs(s0);
                 ab1 += fabs(s1);
             } else {
                 ab0 += fabs(s0) * (1.0 - a.d);
                 ab1 += fabs(s1) * (1.0 - a.d);
-                steps += deg;
+                if (lane == 0) steps += deg;
                 const double w = a.d / (double)deg;
                 const double p0 = s0 * w, p1 = s1 * w;  // sent*(d/deg), engine.py:321
                 for (u32 k0 = 0; k0 < deg; k0 += 32) {
@@ -465,7 +466,8 @@ extern "C" int fr_ppr_run(fr_ppr *p, void *stream, fr_solve_stats *h_stats, doub
     }
     if (h_col_residual)
         for (int col = 0; col < p->B; col++) h_col_residual[col] = c.exact[col];
-    if (c.active) {
+    // an explicit sweep budget is a normal stop (as fr_solver_run); only the implicit cap is an error
+    if (c.active && p->cfg.max_sweeps <= 0) {
         set_error("batched PPR: %d columns did not converge within the sweep budget", __builtin_popcountll(c.active));
         return FR_ERR_NO_CONVERGENCE;
     }

@@ -1,6 +1,6 @@
 // fr_spmv.cu -- power iteration (MAT-ITER), the in-repo comparison solver.
 //
-// baseline.py:181-217: x <- v; repeat y = d*P*x + (1-d)*v; y += (1 - sum y)*v;
+// baseline.py:20-56: x <- v; repeat y = d*P*x + (1-d)*v; y += (1 - sum y)*v;
 // diff = |y - x|_1; x = y; until diff*d/(1-d) <= target.  P*x is a pull SpMV
 // over the transposed CSR (rows = targets, columns = sources ascending, the
 // reference's graph.to_matrix(), graph.py:158-165):
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(PI_NT) k_pi_mass(PiArgs a) {
     t = block_sum<PI_NT>(t, sm);
     if (threadIdx.x == 0) {
         const double ysum = a.d * t + (1.0 - a.d) * a.ctl->sum_v;
-        a.ctl->c = 1.0 - ysum;  // baseline.py:206 dangling mass back through v
+        a.ctl->c = 1.0 - ysum;  // baseline.py:45 dangling mass back through v
     }
 }
 

@@ -42,6 +42,21 @@ __global__ void __launch_bounds__(RED_NT) k_sum_parts(const double *__restrict__
     if (threadIdx.x == 0) *out = s;
 }
 
+// sum |x_i / total - ref_i| (engine.py:271-274: the trace's true L1 error of the
+// normalized history); total = *d_total, 0 means "x is not normalized" (x used as is)
+__global__ void __launch_bounds__(RED_NT) k_err_partials(long long n, const double *__restrict__ x,
+                                                         const double *__restrict__ ref, const double *d_total,
+                                                         double *__restrict__ part) {
+    __shared__ double sm[RED_NT / 32];
+    const double t = *d_total;
+    const double inv = t > 0.0 ? 1.0 / t : 1.0;
+    double s = 0.0;
+    for (long long i = blockIdx.x * (long long)RED_NT + threadIdx.x; i < n; i += (long long)gridDim.x * RED_NT)
+        s += fabs(x[i] * inv - ref[i]);
+    s = block_sum<RED_NT>(s, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 __global__ void k_scale(long long n, const double *__restrict__ x, const double *total, double *__restrict__ y) {
     const double t = *total;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -108,9 +123,36 @@ int abs_sum_async(long long n, const void *x, int fp32, double *d_out, cudaStrea
     return FR_OK;
 }
 
+// |x/|x|_1 - ref|_1 into the device double *d_out, stream-ordered.
+int l1_error_async(long long n, const double *x, const double *ref, double *d_out, cudaStream_t st) {
+    double *part;
+    FR_TRY(reduce_scratch(st, &part));
+    const int g = reduce_grid(n);
+    if ((size_t)g + 2 > SCRATCH_DOUBLES) { set_error("reduction scratch too small"); return FR_ERR_ARG; }
+    double *d_total = part + SCRATCH_DOUBLES - 2;
+    FR_TRY(abs_sum_async(n, x, 0, d_total, st));
+    k_err_partials<<<g, RED_NT, 0, st>>>(n, x, ref, d_total, part);
+    k_sum_parts<<<1, RED_NT, 0, st>>>(part, g, d_out);
+    FR_CUDA(cudaGetLastError());
+    return FR_OK;
+}
+
 }  // namespace fr
 
 using namespace fr;
+
+extern "C" int fr_l1_error(int64_t n, const double *d_history, const double *d_reference, double *h_err,
+                           void *stream) {
+    if (n < 1 || !d_history || !d_reference || !h_err) { set_error("fr_l1_error: bad arguments"); return FR_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    double *part;
+    FR_TRY(reduce_scratch(st, &part));
+    double *d_out = part + SCRATCH_DOUBLES - 1;
+    FR_TRY(l1_error_async(n, d_history, d_reference, d_out, st));
+    FR_CUDA(cudaMemcpyAsync(h_err, d_out, sizeof(double), cudaMemcpyDeviceToHost, st));
+    FR_CUDA(cudaStreamSynchronize(st));
+    return FR_OK;
+}
 
 extern "C" int fr_init_state(int64_t n, double damping, const double *d_teleport, void *d_fluid, int32_t fluid_fp32,
                              double *d_history, void *stream) {

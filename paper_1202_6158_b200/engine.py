@@ -3,7 +3,8 @@
 Same names, argument meaning and errors as the reference; the state vectors
 live in HBM as torch tensors and run() drives the device sweep solver of
 csrc/fr_diffuse.cu (whole convergence loop inside one CUDA graph).  The
-returned rank is a device float64 tensor (``rank.cpu().numpy()`` for numpy).
+returned rank is a numpy float64 vector like the reference's; pass
+``as_tensor=True`` to keep it on the device.
 """
 
 from __future__ import annotations
@@ -18,7 +19,7 @@ import torch
 
 from . import _lib
 from ._lib import check, lib, ptr, require_device, stream_ptr
-from .sched import DeviceSchedule
+from .sched import KINDS, DeviceSchedule
 
 
 class StarvationError(RuntimeError):
@@ -91,6 +92,7 @@ class ConvergenceTrace:
 
     def __init__(self):
         self.rows = []
+        self.sweep_rows = []  # device runs: (elementary_steps, diffusions, residual, bound) per sweep
 
     def append(self, elementary_steps, diffusions, residual, bound, true_error=None, sweeps=0, theta=None):
         self.rows.append(TraceRow(int(elementary_steps), int(diffusions), float(residual),
@@ -294,51 +296,164 @@ def _normalized(history):
     return rank
 
 
+def _true_error(history, ref):
+    """|history/|history|_1 - ref|_1 on the device (engine.py:269-274); None before any mass."""
+    out = ctypes.c_double(0.0)
+    check(lib.fr_l1_error(history.numel(), ptr(history), ptr(ref), ctypes.byref(out), stream_ptr()))
+    return out.value if float(history.abs().sum()) > 0.0 else None
+
+
+def device_schedule(scheduler):
+    """The device sweep rule for a scheduler object, or None for a custom next() rule.
+
+    Accepts this package's DeviceSchedule and any object carrying the reference's
+    ``kind`` attribute (sched.py:16-161: the reference classes, with their ``decay``
+    and ``seed``); objects without a known kind but with next(state, graph) are
+    driven one node at a time like the reference loop (engine.py:297).
+    """
+    if isinstance(scheduler, DeviceSchedule):
+        return scheduler
+    kind = getattr(scheduler, "kind", None)
+    if kind in KINDS:
+        kw = {}
+        if kind == "sweep":
+            kw["decay"] = float(getattr(scheduler, "decay", 0.5))
+        if kind == "rand":
+            seed = getattr(scheduler, "seed", 0)
+            kw["seed"] = int(seed) if isinstance(seed, (int, np.integer)) else 0
+        return DeviceSchedule(kind, **kw)
+    if callable(getattr(scheduler, "next", None)):
+        return None
+    raise TypeError(f"scheduler {scheduler!r} has neither a known kind ({', '.join(KINDS)}) nor next(state, graph)")
+
+
+def _output(rank, as_tensor):
+    return rank if as_tensor else rank.cpu().numpy()
+
+
+def _run_custom(graph, params, scheduler, state, trace, threshold, trace_every, ref, max_diffusions):
+    """engine.py:289-336 for a scheduler with only next(state, graph): the reference
+    loop, one device diffusion per selection, with its starvation bookkeeping."""
+    n, d = graph.n, params.damping
+    stamp = np.zeros(n, dtype=np.int64)
+    epoch, distinct_empty, empty_streak, streak_cap = 1, 0, 0, 64 * n
+    next_trace = state.diffusions + trace_every
+    next_refresh = state.diffusions + n
+
+    def sample():
+        err = None if ref is None else _true_error(state.history, ref)
+        trace.append(state.elementary_steps, state.diffusions, state.residual,
+                     None if d >= 1.0 else state.residual / (1.0 - d), err, sweeps=state.sweeps)
+
+    while True:
+        if state.residual <= threshold:
+            state.residual = state.exact_residual()
+            if state.residual <= threshold:
+                break
+        if max_diffusions is not None and state.diffusions >= max_diffusions:
+            break
+        i = int(scheduler.next(state, graph))
+        before = state.diffusions
+        diffuse(state, i, graph, params)
+        if state.diffusions == before:  # the node held no fluid
+            empty_streak += 1
+            if stamp[i] != epoch:
+                stamp[i] = epoch
+                distinct_empty += 1
+            if distinct_empty >= n or empty_streak >= streak_cap:
+                state.residual = state.exact_residual()
+                if state.residual <= threshold:
+                    break
+                raise StarvationError(
+                    f"scheduler made {empty_streak} empty selections covering {distinct_empty} nodes while "
+                    f"bound {error_bound(state, params):.3g} exceeds target {params.target_error:.3g}")
+            continue
+        empty_streak = distinct_empty = 0
+        epoch += 1
+        if state.diffusions >= next_refresh:
+            state.residual = state.exact_residual()
+            next_refresh = state.diffusions + n
+        if state.diffusions >= next_trace:
+            sample()
+            next_trace = state.diffusions + trace_every
+
+
 def run(graph, params, scheduler, trace_every=None, reference=None, max_diffusions=None, state=None,
-        fluid_dtype=torch.float64, max_sweeps=0):
+        fluid_dtype=torch.float64, max_sweeps=0, as_tensor=False):
     """Diffuse until residual/(1-d) <= target_error (engine.py:240-341).
 
-    Returns (rank, trace): rank is the history renormalized to sum one (a
-    device float64 tensor), trace has one row per device sweep.  With
-    damping=1.0 max_diffusions is required.  trace_every is accepted for
-    signature compatibility; the device records every sweep.
+    Returns (rank, trace): rank is the history renormalized to sum one, a numpy
+    float64 vector like the reference's (``as_tensor=True``: the device tensor,
+    no copy).  The device solves whole sweeps, so trace rows are sampled at
+    sweep ends: a row once the diffusion count has advanced by trace_every
+    (default n, as the reference) since the last one, plus the first and last
+    rows; ``trace.sweep_rows`` keeps one row per sweep.  With ``reference`` (a
+    normalized rank vector) every sampled row carries the true L1 error, taken
+    on the device at that sweep (fr_solver_run_sampled).  With damping=1.0
+    max_diffusions is required.
     """
     params.validate(graph.n)
     d = params.damping
+    n = graph.n
     if d >= 1.0 and max_diffusions is None:
         raise ValueError("undamped diagnostic mode requires max_diffusions")
-    if not isinstance(scheduler, DeviceSchedule):
-        kind = getattr(scheduler, "kind", None)
-        if kind is None:
-            raise ValueError("scheduler must come from make_scheduler (a device selection rule)")
-        scheduler = DeviceSchedule(kind)
+    sched = device_schedule(scheduler)
     if state is None:
         state = init(graph, params, fluid_dtype=fluid_dtype)
-    trace = ConvergenceTrace()
-    bound0 = None if d >= 1.0 else state.residual / (1.0 - d)
-    trace.append(state.elementary_steps, state.diffusions, state.residual, bound0, sweeps=state.sweeps)
-    solver = Solver(graph, state, scheduler, params, max_sweeps=max_sweeps,
-                    max_diffusions=None if max_diffusions is None else max_diffusions - state.diffusions)
-    try:
-        stats = solver.run()
-        base_steps, base_diff, base_sweeps = state.elementary_steps, state.diffusions, state.sweeps
-        for r in solver.trace_rows():
-            trace.append(base_steps + r.elementary_steps, base_diff + r.diffusions, r.residual,
-                         None if d >= 1.0 else r.residual / (1.0 - d), sweeps=base_sweeps + r.sweeps,
-                         theta=r.theta)
-    finally:
-        solver.close()
-    state.elementary_steps += int(stats.elementary_steps)
-    state.diffusions += int(stats.diffusions)
-    state.sweeps += int(stats.sweeps)
-    state.residual = float(stats.residual)
-    rank = _normalized(state.history)
-    err = None
+    trace_every = n if trace_every is None else max(1, int(trace_every))
+    ref = None
     if reference is not None:
-        ref = torch.as_tensor(reference, dtype=torch.float64).to(rank.device)
-        err = float((rank - ref).abs().sum())
-    last = trace.rows[-1]
-    if last.diffusions != state.diffusions or last.residual != state.residual or err is not None:
-        trace.append(state.elementary_steps, state.diffusions, state.residual,
-                     None if d >= 1.0 else state.residual / (1.0 - d), err, sweeps=state.sweeps)
-    return rank, trace
+        ref = torch.as_tensor(np.asarray(reference, dtype=np.float64) if not isinstance(reference, torch.Tensor)
+                              else reference, dtype=torch.float64).to(state.history.device).contiguous()
+        if tuple(ref.shape) != (n,):
+            raise ValueError(f"reference length {tuple(ref.shape)} does not match n={n}")
+    trace = ConvergenceTrace()
+
+    def bound(r):
+        return None if d >= 1.0 else r / (1.0 - d)
+
+    err0 = None if ref is None else _true_error(state.history, ref)
+    trace.append(state.elementary_steps, state.diffusions, state.residual, bound(state.residual), err0,
+                 sweeps=state.sweeps)
+    if sched is None:
+        _run_custom(graph, params, scheduler, state, trace, params.target_error * (1.0 - d), trace_every, ref,
+                    max_diffusions)
+        state.residual = state.exact_residual()
+    else:
+        solver = Solver(graph, state, sched, params, max_sweeps=max_sweeps,
+                        max_diffusions=None if max_diffusions is None else max_diffusions - state.diffusions)
+        try:
+            if ref is None:
+                stats = solver.run()
+                errs = None
+            else:
+                stats = _lib.SolveStats()
+                check(lib.fr_solver_run_sampled(solver.handle, stream_ptr(), ptr(ref), int(trace_every),
+                                                ctypes.byref(stats)))
+                errs = (ctypes.c_double * solver.trace_cap)()
+                check(lib.fr_solver_trace_errors(solver.handle, errs, solver.trace_cap, stream_ptr()))
+            base_steps, base_diff, base_sweeps = state.elementary_steps, state.diffusions, state.sweeps
+            next_trace = base_diff + trace_every
+            for k, r in enumerate(solver.trace_rows()):
+                steps, diffs = base_steps + r.elementary_steps, base_diff + r.diffusions
+                row = (steps, diffs, r.residual, bound(r.residual))
+                trace.sweep_rows.append(row)
+                if diffs >= next_trace:
+                    e = None if errs is None or math.isnan(errs[k]) else float(errs[k])
+                    trace.append(*row, e, sweeps=base_sweeps + r.sweeps, theta=r.theta)
+                    next_trace = diffs + trace_every
+        finally:
+            solver.close()
+        state.elementary_steps += int(stats.elementary_steps)
+        state.diffusions += int(stats.diffusions)
+        state.sweeps += int(stats.sweeps)
+        state.residual = float(stats.residual)
+    rank = _normalized(state.history)
+    err = None if ref is None else float((rank - ref).abs().sum())
+    # the final sample (engine.py:338-340), with the exact residual: it restates a
+    # row already taken at the same diffusion count
+    if trace.rows and trace.rows[-1].diffusions == state.diffusions:
+        trace.rows.pop()
+    trace.append(state.elementary_steps, state.diffusions, state.residual, bound(state.residual), err,
+                 sweeps=state.sweeps)
+    return _output(rank, as_tensor), trace

@@ -73,7 +73,7 @@ def generate(cfg, n, seed=0):
     src, dst = generate_edges(cfg, n, seed)
     off, tgt, (L, dups, loops) = csr_build(n, src, dst, clean=True)
     del src, dst
-    g = SparseGraph(n, off, tgt)
+    g = SparseGraph(n, off, tgt, _trusted=True)
     rep = GenReport(slots=L + dups + loops, realized_links=L, duplicates=dups, self_loops=loops,
                     dangling=g.dangling_count, seed=seed)
     return g, rep
@@ -86,7 +86,7 @@ def baseline_graph(config_index, seed=0, n=None):
 
 
 def degree_report(graph):
-    """Exact in/out degree histograms as {degree: count} (gen.py:577-584)."""
+    """Exact in/out degree histograms as {degree: count} (gen.py:113-120)."""
     out_hist = torch.bincount(graph.out_degree).cpu().numpy()
     in_hist = torch.bincount(graph.in_degree).cpu().numpy()
     return {"out": {int(d): int(c) for d, c in enumerate(out_hist) if c},

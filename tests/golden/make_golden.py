@@ -118,7 +118,7 @@ def run_case(out, tag, g, target_error, teleport=None, kinds=KINDS, damping=0.85
 
 
 def small_runs():
-    """engine.run for every deterministic scheduler + power_iterate (engine.py:240, baseline.py:181)."""
+    """engine.run for every deterministic scheduler + power_iterate (engine.py:240, baseline.py:20)."""
     out = {}
     tags = []
     G = graph.SparseGraph.from_edges
@@ -144,7 +144,7 @@ def small_runs():
                 tel = None
         run_case(out, f"rg{k}", g, 1e-10 if k % 2 else 1e-9, teleport=tel)
         tags.append(f"rg{k}")
-    # the paper's section-4.1 scenario generator (gen.py:530), two scaled scenarios
+    # the paper's section-4.1 scenario generator (gen.py:66), two scaled scenarios
     for k, (n, links, alpha) in enumerate([(600, 1500, 2.0), (800, 5000, 1.5)]):
         g, _ = gen.generate(gen.GenConfig(n=n, links=links, alpha=alpha, seed=31 + k))
         run_case(out, f"paper{k}", g, 1e-9)

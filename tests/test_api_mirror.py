@@ -120,6 +120,49 @@ class TestSchedulerChoices:
         assert sched.DegreeScaledScheduler(use_in_degree=False).kind == "op2"
 
 
+class TestSchedulerProtocol:
+    """run() takes reference scheduler objects (sched.py:16-161) by their kind and knobs."""
+
+    def test_reference_objects_map_to_device_rules(self):
+        from paper_1202_6158_b200.engine import device_schedule
+
+        class ThresholdSweepScheduler:  # the reference class's public attributes
+            kind = "sweep"
+
+            def __init__(self, decay=0.5):
+                self.decay = decay
+
+            def next(self, state, graph):
+                raise AssertionError("the device rule replaces next()")
+
+        class RandomScheduler:
+            kind = "rand"
+
+            def __init__(self, seed=0):
+                self.seed = seed
+
+        s = device_schedule(ThresholdSweepScheduler(decay=0.9))
+        assert (s.kind, s.decay) == ("sweep", 0.9)
+        r = device_schedule(RandomScheduler(seed=11))
+        assert (r.kind, r.seed) == ("rand", 11)
+
+        class DegreeScaled:
+            kind = "op2"
+
+        assert device_schedule(DegreeScaled()).kind == "op2"
+
+    def test_custom_next_and_rejection(self):
+        from paper_1202_6158_b200.engine import device_schedule
+
+        class Custom:
+            def next(self, state, graph):
+                return 0
+
+        assert device_schedule(Custom()) is None
+        with pytest.raises(TypeError):
+            device_schedule(object())
+
+
 class TestTraceObject:
     def test_csv_header_and_rows(self):
         from paper_1202_6158_b200 import ConvergenceTrace
@@ -419,6 +462,56 @@ class TestTrace:
         assert trace.rows[-1].true_error <= params.target_error
         assert trace.steps_to_error(1.0) is not None
 
+    @pytest.mark.parametrize("small", ["1", "0"])
+    def test_sampled_true_errors(self, cuda, monkeypatch, small):
+        """trace_every + reference (engine.py:265-277, 334-336): sampled rows at least
+        trace_every diffusions apart, each with the device-measured true L1 error."""
+        monkeypatch.setenv("FR_SMALL", small)
+        from oracle import oracle as O
+        O.build()
+        n = 5000
+        src, dst = O.gen_edges(O.web_config(8.0), n, 4)
+        off, tgt, _ = O.csr_build(n, src, dst, clean=True)
+        g = cuda.SparseGraph(n, off, tgt.astype(np.int32))
+        truth = O.run_seq(off, tgt, 0.85, 1e-14, "sweep").rank
+        params = cuda.DiffusionParams(target_error=1e-10)
+        rank, trace = cuda.run(g, params, cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.7),
+                               trace_every=n // 2, reference=truth)
+        rows = trace.rows
+        assert len(rows) >= 4
+        assert all(b.diffusions - a.diffusions >= n // 2 for a, b in zip(rows[1:-2], rows[2:-1]))
+        errs = [r.true_error for r in rows[1:]]
+        assert all(e is not None for e in errs)
+        assert errs[-1] == pytest.approx(float(np.abs(rank - truth).sum()), abs=1e-15)
+        assert errs[-1] <= 1e-9 and errs[0] > errs[-1]
+        assert trace.sweep_rows and len(trace.sweep_rows) >= len(rows) - 2
+
+    def test_custom_scheduler_runs_reference_loop(self, cuda, two_cycle):
+        """A scheduler with only next(state, graph) is driven node by node (engine.py:289-336)."""
+        class Alternate:
+            def __init__(self):
+                self.k = 0
+
+            def next(self, state, graph):
+                self.k += 1
+                return self.k % graph.n
+
+        params = cuda.DiffusionParams(target_error=1e-6)
+        rank, trace = cuda.run(two_cycle, params, Alternate(), trace_every=1)
+        assert np.abs(rank - 0.5).sum() <= 2e-6
+        assert len(trace.rows) > 10 and trace.rows[-1].bound <= 1e-6
+
+    def test_custom_scheduler_starvation(self, cuda):
+        """A scheduler that keeps picking an empty node raises StarvationError (engine.py:304-312)."""
+        class Stuck:
+            def next(self, state, graph):
+                return 2
+
+        g = cuda.SparseGraph.from_edges(3, [0, 1], [1, 0])
+        params = cuda.DiffusionParams(teleport=np.array([0.5, 0.5, 0.0]))
+        with pytest.raises(cuda.StarvationError):
+            cuda.run(g, params, Stuck())
+
     def test_signed_state_residual(self, cuda):
         g = cuda.SparseGraph.from_edges(2, [0, 1], [1, 0])
         s = cuda.init_from_fluid(g, cuda.DiffusionParams(), np.array([0.5, -0.25]))
@@ -480,6 +573,19 @@ class TestLoadEdgeList:
 
 @pytest.mark.gpu
 class TestColumn:
+    def test_malformed_csr_rejected(self, cuda):
+        """A caller-supplied CSR is validated once on the device before any kernel indexes it."""
+        with pytest.raises(ValueError):
+            cuda.SparseGraph(2, np.array([0, 1, 3]), np.array([1, 0]))  # off[n] != len(targets)
+        with pytest.raises(ValueError):
+            cuda.SparseGraph(3, np.array([0, 2, 1, 2]), np.array([1, 2]))  # decreasing offsets
+        with pytest.raises(ValueError):
+            cuda.SparseGraph(2, np.array([0, 1, 2]), np.array([1, 2]))  # target >= n
+        with pytest.raises(ValueError):
+            cuda.SparseGraph(2, np.array([1, 1, 2]), np.array([1, 0]))  # off[0] != 0
+        g = cuda.SparseGraph(2, np.array([0, 1, 2]), np.array([1, 0]))
+        assert g.edge_count == 2
+
     def test_two_cycle(self, cuda, two_cycle):
         assert two_cycle.column(0) == [(1, 1.0)]
 

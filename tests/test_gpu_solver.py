@@ -188,7 +188,7 @@ def test_zero_edge_graph_converges_to_teleport(cuda):
     g = cuda.SparseGraph.from_edges(3, [], [])
     v = np.array([0.2, 0.3, 0.5])
     rank, _ = cuda.run(g, cuda.DiffusionParams(teleport=v), cuda.make_scheduler("sweep"))
-    assert np.allclose(rank.cpu().numpy(), v, atol=1e-12)
+    assert np.allclose(rank, v, atol=1e-12)
 
 
 def test_undamped_diagnostic_mode(cuda):
@@ -197,7 +197,7 @@ def test_undamped_diagnostic_mode(cuda):
         cuda.run(g, cuda.DiffusionParams(damping=1.0), cuda.make_scheduler("max"))
     rank, trace = cuda.run(g, cuda.DiffusionParams(damping=1.0), cuda.make_scheduler("sweep"), max_diffusions=500)
     assert trace.rows[-1].diffusions >= 500
-    assert np.allclose(rank.cpu().numpy(), [0.5, 0.5], atol=2e-3)
+    assert np.allclose(rank, [0.5, 0.5], atol=2e-3)
 
 
 def test_signed_fluid_resume(cuda, oracle):
@@ -225,9 +225,40 @@ def test_host_buffer_entry_point(cuda, golden_configs):
     cfg = cuda.make_scheduler("sweep").solver_config(cuda.DiffusionParams(target_error=1e-10))
     rank = np.empty(n)
     stats = _lib.SolveStats()
-    _lib.check(_lib.lib.fr_pagerank_host(n, tgt.size, off.ctypes.data, tgt.ctypes.data, ctypes.byref(cfg),
+    _lib.check(_lib.lib.fr_pagerank_host(n, tgt.size, off.ctypes.data, tgt.ctypes.data, None, ctypes.byref(cfg),
                                          rank.ctypes.data, ctypes.byref(stats)))
     assert l1(rank, golden_configs["cfg1_sweep_rank"]) <= L1_FP64
+
+
+@pytest.mark.parametrize("n,mean", [(5_000, 8.0), (300_000, 12.0)])
+def test_host_buffer_entry_point_teleport(cuda, oracle, n, mean):
+    """fr_pagerank_host with a personalized teleport (params.teleport, engine.py:56-62,
+    149-159) against the oracle run with the same V; bad vectors are rejected like
+    DiffusionParams.validate (engine.py:47-54)."""
+    import ctypes
+    from paper_1202_6158_b200 import _lib
+    src, dst = oracle.gen_edges(oracle.web_config(mean), n, 23)
+    off, tgt, _ = oracle.csr_build(n, src, dst, clean=True)
+    rng = np.random.default_rng(5)
+    v = np.zeros(n)
+    v[rng.choice(n, 50, replace=False)] = rng.uniform(0.5, 1.5, 50)
+    v /= v.sum()
+    params = cuda.DiffusionParams(target_error=1e-10, teleport=v)
+    cfg = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.6, edge_frac=0.2,
+                              degree_exponent=0.65).solver_config(params)
+    rank = np.empty(n)
+    stats = _lib.SolveStats()
+    _lib.check(_lib.lib.fr_pagerank_host(n, tgt.size, off.ctypes.data, tgt.ctypes.data, v.ctypes.data,
+                                         ctypes.byref(cfg), rank.ctypes.data, ctypes.byref(stats)))
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-12, "sweep", teleport=v).rank
+    assert l1(rank, ref) <= L1_FP64
+    uniform = oracle.run_seq(off, tgt, 0.85, 1e-10, "sweep").rank
+    assert l1(rank, uniform) > 1e-3  # the teleport was used
+    for bad in (v * 1.001, np.where(np.arange(n) == 0, -1e-3, v)):
+        bad = np.ascontiguousarray(bad)
+        with pytest.raises(ValueError):
+            _lib.check(_lib.lib.fr_pagerank_host(n, tgt.size, off.ctypes.data, tgt.ctypes.data, bad.ctypes.data,
+                                                 ctypes.byref(cfg), rank.ctypes.data, ctypes.byref(stats)))
 
 
 @pytest.mark.parametrize("hot_slots,warm_slots", [(-1, -1), (0, -1), (7, 0), (0, 0), (-1, 5000)])
@@ -259,7 +290,7 @@ def test_host_buffer_entry_point_with_hubs(cuda, oracle):
     for _ in range(2):
         rank = np.empty(n)
         stats = _lib.SolveStats()
-        _lib.check(_lib.lib.fr_pagerank_host(n, tgt.size, off.ctypes.data, tgt.ctypes.data, ctypes.byref(cfg),
+        _lib.check(_lib.lib.fr_pagerank_host(n, tgt.size, off.ctypes.data, tgt.ctypes.data, None, ctypes.byref(cfg),
                                              rank.ctypes.data, ctypes.byref(stats)))
         ref = oracle.run_seq(off, tgt, 0.85, 1e-11, "sweep").rank
         assert l1(rank, ref) <= 1e-9
@@ -418,3 +449,27 @@ def test_small_graph_single_launch(cuda, oracle, monkeypatch, small):
     p = oracle.run_psweep(off, tgt, 0.85, 1e-10, policy=2, decay=0.7, weight=(deg + 1.0) ** -0.65,
                           edge_frac=0.15)
     assert trace.rows[-1].elementary_steps <= 1.05 * p.elementary_steps
+
+
+@pytest.mark.parametrize("path,small", [("owned", "1"), ("owned", "0"), ("fused", "0")])
+def test_signed_fluid_residual_refresh(cuda, oracle, monkeypatch, path, small):
+    """Signed fluid whose pushes cancel: the true |F|_1 falls much faster than the incremental
+    estimate R - (1-d)|sent|, so without the reference's periodic exact refresh (every n
+    diffusions, engine.py:331-333) the loop would sweep on until the fluid underflows. The
+    device re-derives R every n diffusions and stops at the target like the reference."""
+    monkeypatch.setenv("FR_SMALL", small)
+    n = 4000
+    src = np.repeat(np.arange(n), 2)
+    dst = (src + np.tile([1, 2], n)) % n
+    g = cuda.SparseGraph.from_edges(n, src, dst)
+    f0 = np.where(np.arange(n) % 2 == 0, 1.0, -1.0) / n
+    params = cuda.DiffusionParams(target_error=1e-10)
+    sched = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.7, kernel_path=path)
+    state = cuda.init_from_fluid(g, params, f0)
+    assert state.signed
+    cuda.run(g, params, sched, state=state)
+    assert state.residual <= 1e-10 * 0.15
+    assert state.sweeps < 400, state.sweeps
+    off, tgt, _ = oracle.csr_build(n, src.astype(np.uint32), dst.astype(np.uint32), clean=False)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-13, "sweep", fluid=f0)
+    assert l1(state.history, ref.history) <= 2e-10

@@ -85,4 +85,4 @@ def test_resume_matches_fresh_run(cuda):
         g2 = cuda.apply_delta(g, single_edit(cuda, rng, g))
         resumed, _ = update.resume(state, g2, params, cuda.make_scheduler("sweep"))
         fresh, _ = cuda.run(g2, params, cuda.make_scheduler("sweep"))
-        assert float((resumed - fresh).abs().sum()) <= 2 * params.target_error
+        assert float(np.abs(resumed - fresh).sum()) <= 2 * params.target_error

@@ -42,7 +42,7 @@ def test_parallel_sweep_agrees_with_sequential(oracle):
 
 
 def test_signed_resume_in_oracle(oracle):
-    """Negative fluid diffuses with the same rule (update.py:424-449 path)."""
+    """Negative fluid diffuses with the same rule (update.py:77-102 path)."""
     rng = np.random.default_rng(3)
     n = 200
     src = rng.integers(0, n, 800)

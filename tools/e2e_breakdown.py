@@ -65,7 +65,7 @@ def solve():
 t_solve = timed(solve)
 solver.close()
 stats = _lib.SolveStats()
-t_e2e = timed(lambda: _lib.check(_lib.lib.fr_pagerank_host(n, L, h_off.data_ptr(), h_tgt.data_ptr(),
+t_e2e = timed(lambda: _lib.check(_lib.lib.fr_pagerank_host(n, L, h_off.data_ptr(), h_tgt.data_ptr(), None,
                                                            ctypes.byref(cfg), h_rank.data_ptr(),
                                                            ctypes.byref(stats))))
 print(f"H2D {t_h2d * 1e3:.1f} ms ({(h_off.numel() * 8 + h_tgt.numel() * 4) / t_h2d / 1e9:.1f} GB/s)  "

@@ -47,7 +47,7 @@ for case in range(cases):
     try:
         rank, trace = fr.run(g, params, sched, fluid_dtype=torch.float32 if fp32 else torch.float64)
         ref = oracle.run_seq(off, tgt, damping, target * 1e-3, "sweep").rank
-        err = float(np.abs(rank.cpu().numpy() - ref).sum())
+        err = float(np.abs(rank - ref).sum())
         # the solver's bound: L1 of the normalized rank <= ~2 * target / |h|_1 (fp64); fp32 fluid 1e-6
         bound = 1e-6 if fp32 else 2.5 * target / (1 - damping) + 1e-12
         ok = err <= bound and trace.rows[-1].residual <= target * (1 - damping) * (1 + 1e-9)
