@@ -68,6 +68,17 @@ int fr_gen_degrees(const fr_gen_config *cfg, int64_t n, uint64_t seed, uint32_t 
 /* Source-major edge list (src[e], dst[e]), e < h_total of fr_gen_degrees. */
 int fr_gen_edges(const fr_gen_config *cfg, int64_t n, uint64_t seed, const uint32_t *d_deg,
                  uint32_t *d_src, uint32_t *d_dst, void *stream);
+/* Fill round `round` of the exact-size graph (round 0 = fr_gen_edges): d_deg is
+ * the per-node deficit left by cleaning (duplicates / self-loops dropped) and
+ * (d_offsets, d_targets) the clean graph so far (NULL in round 0); the draws
+ * come from fresh per-round streams, and a node whose local window the graph
+ * already completes draws from the Zipf class only.  Repeating draw -> clean
+ * union until no deficit is left realises the configured out-degrees as
+ * distinct edges, as the reference generator draws until the target count of
+ * distinct links exists (gen.py:66-110). */
+int fr_gen_edges_round(const fr_gen_config *cfg, int64_t n, uint64_t seed, uint32_t round,
+                       const uint32_t *d_deg, const int64_t *d_offsets, const uint32_t *d_targets,
+                       uint32_t *d_src, uint32_t *d_dst, void *stream);
 
 /* ------------------------------------------------------------------ */
 /* CSR construction on the device.                                     */

@@ -207,10 +207,12 @@ int64_t fro_gen_degrees(const fro_gen_config *c, int64_t n, uint64_t seed, uint3
     return total;
 }
 
-/* Target of slot j of source u (web kind needs the zipf table). */
+/* Target of slot j of source u (web kind needs the zipf table).  zipf_only:
+ * the node's local window already holds every id (a fill round), so the
+ * local class is skipped. */
 static inline uint32_t gen_target(const fro_gen_config *c, int64_t n, uint64_t ke, uint64_t kz,
                                   const double *zcdf, const uint64_t fk[4], int half,
-                                  uint32_t lthr, int64_t u, int64_t j)
+                                  uint32_t lthr, int64_t u, int64_t j, int zipf_only)
 {
     uint64_t r = frand(ke, (uint64_t)u, (uint64_t)j);
     if (c->kind == 0) {
@@ -218,7 +220,7 @@ static inline uint32_t gen_target(const fro_gen_config *c, int64_t n, uint64_t k
         if (t >= (uint64_t)u) t++;
         return (uint32_t)t;
     }
-    if ((uint32_t)(r >> 32) < lthr) {
+    if (!zipf_only && (uint32_t)(r >> 32) < lthr) {
         uint32_t w2 = 2u * (uint32_t)c->window;
         int64_t o = (int64_t)((uint32_t)r % w2);
         int64_t off = o < c->window ? o - c->window : o - c->window + 1;
@@ -230,12 +232,55 @@ static inline uint32_t gen_target(const fro_gen_config *c, int64_t n, uint64_t k
     return (uint32_t)feistel((uint64_t)rank, (uint64_t)n, fk, half);
 }
 
-/* Edge list in source-major slot order: edges of u occupy
- * [eoff[u], eoff[u] + deg[u]).  src/dst have length sum(deg). */
-int fro_gen_edges(const fro_gen_config *c, int64_t n, uint64_t seed, const uint32_t *deg,
-                  uint32_t *src, uint32_t *dst)
+/* Draw-stream keys of fill round r (fro_gen_edges_round): round 0 is the base
+ * draw; round r > 0 redraws the slots that cleaning dropped (duplicates,
+ * self-loops) from fresh edge / Zipf streams.  The Feistel permutation is a
+ * property of the graph and stays the same in every round. */
+#define FILL_GOLD 0xD1B54A32D192ED03ull
+static void round_keys(uint64_t seed, uint32_t round, uint64_t *ke, uint64_t *kz)
 {
-    uint64_t ke = stream_key(seed, FRO_STREAM_EDGE), kz = stream_key(seed, FRO_STREAM_ZIPF);
+    *ke = stream_key(seed, FRO_STREAM_EDGE);
+    *kz = stream_key(seed, FRO_STREAM_ZIPF);
+    if (round) {
+        *ke = mix64(*ke ^ ((uint64_t)round * FILL_GOLD));
+        *kz = mix64(*kz ^ ((uint64_t)round * FILL_GOLD));
+    }
+}
+
+/* first position in t[lo, hi) holding a value >= x */
+static int64_t lower_u32(const uint32_t *t, int64_t lo, int64_t hi, uint64_t x)
+{
+    while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if ((uint64_t)t[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+/* Ids of node u's local window (u +- window, wrapped, u excluded) present in
+ * its sorted row tgt[lo, hi). */
+static int64_t window_count(const uint32_t *tgt, int64_t lo, int64_t hi, int64_t u, int64_t w, int64_t n)
+{
+    /* count of row entries in [a, b] (inclusive, 0 <= a <= b < n) */
+#define ROW_RANGE(a, b) (lower_u32(tgt, lo, hi, (uint32_t)(b) + 1ull) - lower_u32(tgt, lo, hi, (uint32_t)(a)))
+    if (2 * w + 1 >= n) return hi - lo;  /* the window is every other node */
+    int64_t a = u - w, b = u + w;
+    if (a >= 0 && b < n) return ROW_RANGE(a, b);
+    if (a < 0) return ROW_RANGE(0, b) + ROW_RANGE(a + n, n - 1);
+    return ROW_RANGE(a, n - 1) + ROW_RANGE(0, b - n);
+#undef ROW_RANGE
+}
+
+/* Edge list in source-major slot order: edges of u occupy
+ * [eoff[u], eoff[u] + deg[u]).  src/dst have length sum(deg).  round 0 is the
+ * base draw (fro_gen_edges); deg is then the per-node deficit of a fill round
+ * and (off, tgt) the clean graph so far: a node whose local window is already
+ * complete in it draws its fill slots from the Zipf class only. */
+int fro_gen_edges_round(const fro_gen_config *c, int64_t n, uint64_t seed, uint32_t round, const uint32_t *deg,
+                        const int64_t *off, const uint32_t *tgt, uint32_t *src, uint32_t *dst)
+{
+    uint64_t ke, kz;
+    round_keys(seed, round, &ke, &kz);
     uint64_t fk[4];
     for (int r = 0; r < 4; r++) fk[r] = stream_key(seed, FRO_STREAM_FEISTEL + r);
     int half = feistel_half((uint64_t)n);
@@ -247,14 +292,23 @@ int fro_gen_edges(const fro_gen_config *c, int64_t n, uint64_t seed, const uint3
     }
     uint32_t lthr = frac_to_u32(c->local_frac);
     int64_t e = 0;
+    const int64_t wfull = 2 * (int64_t)c->window < n - 1 ? 2 * (int64_t)c->window : n - 1;
     for (int64_t u = 0; u < n; u++) {
+        if (!deg[u]) continue;
+        const int zonly = c->kind == 1 && off && window_count(tgt, off[u], off[u + 1], u, c->window, n) >= wfull;
         for (int64_t j = 0; j < (int64_t)deg[u]; j++, e++) {
             src[e] = (uint32_t)u;
-            dst[e] = gen_target(c, n, ke, kz, zcdf, fk, half, lthr, u, j);
+            dst[e] = gen_target(c, n, ke, kz, zcdf, fk, half, lthr, u, j, zonly);
         }
     }
     free(zcdf);
     return 0;
+}
+
+int fro_gen_edges(const fro_gen_config *c, int64_t n, uint64_t seed, const uint32_t *deg,
+                  uint32_t *src, uint32_t *dst)
+{
+    return fro_gen_edges_round(c, n, seed, 0, deg, NULL, NULL, src, dst);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -309,6 +363,50 @@ int fro_csr_build(int64_t n, int64_t m, const uint32_t *src, const uint32_t *dst
         }
     }
     off[n] = w;
+    if (stats) { stats[0] = w; stats[1] = dups; stats[2] = loops; }
+    return 0;
+}
+
+/* Clean union of a clean CSR (rows sorted, unique, no self-loops) with extra
+ * edges (src2, dst2): build_clean_edges (graph.py:183-200) of the concatenated
+ * edge list, computed row by row as a merge.  stats = {L, duplicates dropped,
+ * self-loops dropped} of the extra edges. */
+int fro_csr_merge(int64_t n, const int64_t *off, const uint32_t *tgt, int64_t m2, const uint32_t *src2,
+                  const uint32_t *dst2, int64_t *off_out /* n+1 */, uint32_t *tgt_out /* off[n]+m2 */,
+                  int64_t *stats /* 3 */)
+{
+    int64_t *o2 = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    uint32_t *t2 = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(m2 > 0 ? m2 : 1));
+    int64_t *cur = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    if (!o2 || !t2 || !cur) { free(o2); free(t2); free(cur); return -1; }
+    int64_t loops = 0, dups = 0;
+    for (int64_t e = 0; e < m2; e++) {
+        if ((int64_t)src2[e] >= n || (int64_t)dst2[e] >= n) { free(o2); free(t2); free(cur); return 1; }
+        if (src2[e] == dst2[e]) loops++;
+        else o2[src2[e] + 1]++;
+    }
+    for (int64_t i = 0; i < n; i++) o2[i + 1] += o2[i];
+    memcpy(cur, o2, sizeof(int64_t) * (size_t)n);
+    for (int64_t e = 0; e < m2; e++)
+        if (src2[e] != dst2[e]) t2[cur[src2[e]]++] = dst2[e];
+    int64_t w = 0;
+    for (int64_t i = 0; i < n; i++) {
+        int64_t b2 = o2[i], e2 = o2[i + 1];
+        qsort(t2 + b2, (size_t)(e2 - b2), sizeof(uint32_t), cmp_u32);
+        int64_t a = off[i], ae = off[i + 1], k = b2;
+        off_out[i] = w;
+        int64_t row0 = w;
+        while (a < ae || k < e2) {
+            const uint32_t v = (k >= e2 || (a < ae && tgt[a] <= t2[k])) ? tgt[a++] : t2[k++];
+            if (w > row0 && tgt_out[w - 1] == v) {  /* the existing row is unique: a repeat is an extra edge */
+                dups++;
+                continue;
+            }
+            tgt_out[w++] = v;
+        }
+    }
+    off_out[n] = w;
+    free(o2); free(t2); free(cur);
     if (stats) { stats[0] = w; stats[1] = dups; stats[2] = loops; }
     return 0;
 }

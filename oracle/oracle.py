@@ -62,6 +62,10 @@ def lib():
         L.fro_gen_degrees.argtypes = [P, i64, ctypes.c_uint64, P]
         L.fro_gen_edges.restype = i32
         L.fro_gen_edges.argtypes = [P, i64, ctypes.c_uint64, P, P, P]
+        L.fro_gen_edges_round.restype = i32
+        L.fro_gen_edges_round.argtypes = [P, i64, ctypes.c_uint64, ctypes.c_uint32, P, P, P, P, P]
+        L.fro_csr_merge.restype = i32
+        L.fro_csr_merge.argtypes = [i64, P, P, i64, P, P, P, P, P]
         L.fro_gen_feistel.restype = ctypes.c_uint64
         L.fro_gen_feistel.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
         L.fro_gen_powerlaw_table.restype = i32
@@ -114,6 +118,65 @@ def gen_edges(cfg, n, seed):
     if lib().fro_gen_edges(ctypes.byref(cfg), n, seed, _ptr(deg), _ptr(src), _ptr(dst)) != 0:
         raise MemoryError("generator table allocation failed")
     return src, dst
+
+
+def gen_edges_round(cfg, n, seed, rnd, deg, off=None, tgt=None):
+    """Draws for deg[u] slots of every node in fill round rnd (round 0 = gen_edges);
+    (off, tgt): the clean graph so far (a node whose local window it already fills
+    draws from the Zipf class only)."""
+    deg = np.ascontiguousarray(deg, dtype=np.uint32)
+    total = int(deg.sum(dtype=np.int64))
+    src = np.empty(max(total, 1), dtype=np.uint32)
+    dst = np.empty(max(total, 1), dtype=np.uint32)
+    off = None if off is None else np.ascontiguousarray(off, dtype=np.int64)
+    tgt = None if tgt is None else np.ascontiguousarray(tgt, dtype=np.uint32)
+    if lib().fro_gen_edges_round(ctypes.byref(cfg), n, seed, rnd, _ptr(deg), _ptr(off), _ptr(tgt), _ptr(src),
+                                 _ptr(dst)) != 0:
+        raise MemoryError("generator table allocation failed")
+    return src[:total], dst[:total]
+
+
+def csr_merge(n, off, tgt, src2, dst2):
+    """Clean union of a clean CSR with extra edges (graph.py:183-200 on the concatenation)."""
+    src2 = np.ascontiguousarray(src2, dtype=np.uint32)
+    dst2 = np.ascontiguousarray(dst2, dtype=np.uint32)
+    off_out = np.empty(n + 1, dtype=np.int64)
+    tgt_out = np.empty(max(int(off[-1]) + src2.size, 1), dtype=np.uint32)
+    stats = np.zeros(3, dtype=np.int64)
+    rc = lib().fro_csr_merge(n, _ptr(np.ascontiguousarray(off, dtype=np.int64)),
+                             _ptr(np.ascontiguousarray(tgt, dtype=np.uint32)), src2.size, _ptr(src2), _ptr(dst2),
+                             _ptr(off_out), _ptr(tgt_out), _ptr(stats))
+    if rc:
+        raise ValueError(CSR_ERRORS.get(rc, f"csr merge failed ({rc})"))
+    return off_out, tgt_out[: int(stats[0])].copy(), tuple(int(x) for x in stats)
+
+
+MAX_FILL_ROUNDS = 32
+
+
+def gen_graph_exact(cfg, n, seed, max_rounds=MAX_FILL_ROUNDS):
+    """The exact-size BASELINE graph: base draw, cleaned, then fill rounds that redraw the
+    dropped slots (per-node deficit) until every node has its configured out-degree in
+    distinct edges (the reference generator draws until the target number of distinct
+    links exists, gen.py:66-110).  Returns (off, tgt, report dict)."""
+    deg, total = gen_degrees(cfg, n, seed)
+    src, dst = gen_edges_round(cfg, n, seed, 0, deg)
+    off, tgt, (L, dups, loops) = csr_build(n, src, dst, clean=True)
+    del src, dst
+    slots, rounds = total, 0
+    for r in range(1, max_rounds + 1):
+        deficit = (deg.astype(np.int64) - np.diff(off)).astype(np.uint32)
+        need = int(deficit.sum(dtype=np.int64))
+        if need == 0:
+            break
+        s2, d2 = gen_edges_round(cfg, n, seed, r, deficit, off, tgt)
+        off, tgt, (L, rd, rl) = csr_merge(n, off, tgt, s2, d2)
+        slots += need
+        dups += rd
+        loops += rl
+        rounds = r
+    return off, tgt, {"slots": slots, "realized_links": L, "duplicates": dups, "self_loops": loops,
+                      "target_links": total, "rounds": rounds, "unfilled": total - L}
 
 
 def feistel(x, n, seed):

@@ -68,6 +68,7 @@ SIGNATURES = {
     "fr_device_sms": (ctypes.c_int, []),
     "fr_gen_degrees": (ctypes.c_int, [_P, _I64, _U64, _P, _P, _P]),
     "fr_gen_edges": (ctypes.c_int, [_P, _I64, _U64, _P, _P, _P, _P]),
+    "fr_gen_edges_round": (ctypes.c_int, [_P, _I64, _U64, ctypes.c_uint32, _P, _P, _P, _P, _P, _P]),
     "fr_csr_build": (ctypes.c_int, [_I64, _I64, _P, _P, _I32, _P, _P, _P, _P]),
     "fr_in_degree": (ctypes.c_int, [_I64, _I64, _P, _P, _P]),
     "fr_init_state": (ctypes.c_int, [_I64, _F64, _P, _P, _I32, _P, _P]),

@@ -135,14 +135,14 @@ struct EdgeGenArgs {
     const double *zcdf;
 };
 
-__device__ __forceinline__ u32 gen_target(const EdgeGenArgs &a, long long u, long long j) {
+__device__ __forceinline__ u32 gen_target(const EdgeGenArgs &a, long long u, long long j, bool zipf_only) {
     u64 r = frand(a.ke, (u64)u, (u64)j);
     if (a.kind == 0) {
         u64 t = r % (u64)(a.n - 1);
         if (t >= (u64)u) t++;
         return (u32)t;
     }
-    if ((u32)(r >> 32) < a.lthr) {
+    if (!zipf_only && (u32)(r >> 32) < a.lthr) {
         u32 w2 = 2u * (u32)a.window;
         long long o = (long long)((u32)r % w2);
         long long off = o < a.window ? o - a.window : o - a.window + 1;
@@ -154,18 +154,50 @@ __device__ __forceinline__ u32 gen_target(const EdgeGenArgs &a, long long u, lon
     return (u32)feistel((u64)rank, (u64)a.n, a.fk);
 }
 
-// One warp per source node; lanes cover its slots.
+// first position in t[lo, hi) holding a value >= x
+__device__ __forceinline__ long long lower_u32(const u32 *__restrict__ t, long long lo, long long hi, u64 x) {
+    while (lo < hi) {
+        const long long mid = lo + (hi - lo) / 2;
+        if ((u64)t[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Ids of u's local window (u +- w, wrapped, u excluded) present in its sorted row.
+__device__ long long window_count(const u32 *__restrict__ t, long long lo, long long hi, long long u, long long w,
+                                  long long n) {
+    auto range = [&](long long x, long long y) { return lower_u32(t, lo, hi, (u64)y + 1) - lower_u32(t, lo, hi, (u64)x); };
+    if (2 * w + 1 >= n) return hi - lo;
+    const long long x = u - w, y = u + w;
+    if (x >= 0 && y < n) return range(x, y);
+    if (x < 0) return range(0, y) + range(x + n, n - 1);
+    return range(x, n - 1) + range(0, y - n);
+}
+
+// One warp per source node; lanes cover its slots.  Fill rounds pass the clean
+// graph so far (off, tgt): a node whose local window it already completes
+// draws from the Zipf class only.
 __global__ void __launch_bounds__(256) k_gen_edges(EdgeGenArgs a, const u32 *__restrict__ deg,
-                                                   const u64 *__restrict__ eoff, u32 *__restrict__ src,
+                                                   const u64 *__restrict__ eoff, const u64 *__restrict__ off,
+                                                   const u32 *__restrict__ tgt, u32 *__restrict__ src,
                                                    u32 *__restrict__ dst) {
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    const long long wfull = 2ll * a.window < a.n - 1 ? 2ll * a.window : a.n - 1;
     for (long long u = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); u < a.n; u += warps) {
         const long long g = deg[u];
+        if (g == 0) continue;
         const u64 base = eoff[u];
+        bool zonly = false;
+        if (a.kind == 1 && off) {
+            int full = 0;
+            if (lane == 0) full = window_count(tgt, (long long)off[u], (long long)off[u + 1], u, a.window, a.n) >= wfull;
+            zonly = __shfl_sync(0xffffffffu, full, 0) != 0;
+        }
         for (long long j = lane; j < g; j += 32) {
             src[base + j] = (u32)u;
-            dst[base + j] = gen_target(a, u, j);
+            dst[base + j] = gen_target(a, u, j, zonly);
         }
     }
 }
@@ -242,6 +274,17 @@ extern "C" int fr_gen_degrees(const fr_gen_config *c, int64_t n, uint64_t seed, 
 
 extern "C" int fr_gen_edges(const fr_gen_config *c, int64_t n, uint64_t seed, const uint32_t *d_deg,
                             uint32_t *d_src, uint32_t *d_dst, void *stream) {
+    return fr_gen_edges_round(c, n, seed, 0, d_deg, nullptr, nullptr, d_src, d_dst, stream);
+}
+
+// Fill round r > 0 redraws the slots that cleaning dropped (d_deg = per-node
+// deficit) from fresh edge / Zipf streams; the Feistel permutation, a property
+// of the graph, is the same in every round (oracle: fro_gen_edges_round).
+static constexpr u64 FILL_GOLD = 0xD1B54A32D192ED03ull;
+
+extern "C" int fr_gen_edges_round(const fr_gen_config *c, int64_t n, uint64_t seed, uint32_t round,
+                                  const uint32_t *d_deg, const int64_t *d_offsets, const uint32_t *d_targets,
+                                  uint32_t *d_src, uint32_t *d_dst, void *stream) {
     FR_TRY(check_gen_config(c, n));
     cudaStream_t st = (cudaStream_t)stream;
     Scratch scratch(st);
@@ -252,6 +295,10 @@ extern "C" int fr_gen_edges(const fr_gen_config *c, int64_t n, uint64_t seed, co
     a.lthr = frac_to_u32(c->local_frac);
     a.ke = stream_key(seed, STREAM_EDGE);
     a.kz = stream_key(seed, STREAM_ZIPF);
+    if (round) {
+        a.ke = mix64(a.ke ^ ((u64)round * FILL_GOLD));
+        a.kz = mix64(a.kz ^ ((u64)round * FILL_GOLD));
+    }
     for (int r = 0; r < 4; r++) a.fk.k[r] = stream_key(seed, STREAM_FEISTEL + r);
     {
         int bits = 2;
@@ -274,7 +321,8 @@ extern "C" int fr_gen_edges(const fr_gen_config *c, int64_t n, uint64_t seed, co
     FR_TRY(exclusive_scan_u32_to_u64(d_deg, d_eoff, n, st));
     DeviceInfo di;
     FR_TRY(device_info(&di));
-    k_gen_edges<<<di.sms * 8, 256, 0, st>>>(a, d_deg, d_eoff, d_src, d_dst);
+    k_gen_edges<<<di.sms * 8, 256, 0, st>>>(a, d_deg, d_eoff, reinterpret_cast<const u64 *>(d_offsets), d_targets,
+                                            d_src, d_dst);
     FR_CUDA(cudaGetLastError());
     FR_CUDA(cudaStreamSynchronize(st));  // host table z must outlive the upload
     return FR_OK;

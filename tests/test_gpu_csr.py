@@ -131,3 +131,20 @@ def test_apply_delta_and_delta_columns(cuda):
     assert cuda.delta_columns(g, g3) == []
     with pytest.raises(cuda.DeltaError):
         cuda.apply_delta(g, cuda.GraphDelta(added=[(0, 1)], removed=[]))
+
+
+@pytest.mark.parametrize("kind,n,seed", [("uniform", 10_000, 1234), ("web8", 70_000, 2), ("web16", 300_000, 0)])
+def test_exact_size_generator_bit_exact(cuda, oracle, kind, n, seed):
+    """gen.generate(exact=True) -- base draw, cleaned, then fill rounds redrawing the dropped
+    slots on the device -- is bit-exact with the oracle's gen_graph_exact, report included."""
+    from paper_1202_6158_b200 import gen
+    g, rep = gen.generate({"uniform": gen.uniform_config(10), "web8": gen.web_config(8.0),
+                           "web16": gen.web_config(16.0)}[kind], n, seed, exact=True)
+    ocfg = {"uniform": oracle.uniform_config(10), "web8": oracle.web_config(8.0),
+            "web16": oracle.web_config(16.0)}[kind]
+    off, tgt, orep = oracle.gen_graph_exact(ocfg, n, seed)
+    assert np.array_equal(to_np(g.out_offsets), off)
+    assert np.array_equal(to_np(g.out_targets).astype(np.uint32), tgt)
+    assert (rep.slots, rep.realized_links, rep.duplicates, rep.self_loops, rep.target_links, rep.rounds,
+            rep.unfilled) == (orep["slots"], orep["realized_links"], orep["duplicates"], orep["self_loops"],
+                              orep["target_links"], orep["rounds"], orep["unfilled"])
