@@ -105,6 +105,7 @@ def generate(cfg, n, seed=0, exact=False, max_rounds=MAX_FILL_ROUNDS):
     src, dst = draw_edges(cfg, n, seed, deg, total, 0)
     off, tgt, (L, dups, loops) = csr_build(n, src, dst, clean=True)
     del src, dst
+    torch.cuda.empty_cache()
     slots, rounds = total, 0
     if exact:
         deg64 = deg.to(torch.int64)
@@ -118,10 +119,15 @@ def generate(cfg, n, seed=0, exact=False, max_rounds=MAX_FILL_ROUNDS):
             # clean union of the graph so far with the redraws: one device CSR build
             rows = torch.repeat_interleave(torch.arange(n, dtype=torch.int32, device=off.device), torch.diff(off))
             src = torch.cat([rows, s2])
+            del rows, s2
             dst = torch.cat([tgt, d2])
-            del rows, s2, d2
+            del off, tgt, d2, d32, deficit
+            # the builder allocates from the CUDA stream-ordered pool: hand torch's cached
+            # blocks back first (config 5: 1.6B edges, ~13 GB per edge-list copy)
+            torch.cuda.empty_cache()
             off, tgt, (L, rd, rl) = csr_build(n, src, dst, clean=True)
             del src, dst
+            torch.cuda.empty_cache()
             slots += need
             dups += rd
             loops += rl
