@@ -12,7 +12,9 @@ so --gpus N runs N independent replicas ("replicas only", scaling = weak).
 
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port of engine.run + ThresholdSweepScheduler, bit-exact with the
-reference) on a bounded sample of the workload, on the host cores.
+reference) on the same config-5 graph (built by the oracle's generator, bit-
+exact with the device's), each step a bounded sample: the sequential run from
+the initial state for a fixed diffusion budget.
 """
 
 from __future__ import annotations
@@ -42,7 +44,8 @@ WORKLOADS = {
     2: dict(n=1_000_000, mean=8.0, damping=0.85, target=1e-9,
             name="config2: web graph N=1M, mean out-degree 8, d=0.85, fp64, L1 residual 1e-9"),
 }
-CPU_SAMPLE_N = 1_000_000
+CPU_SAMPLE_DIFFUSIONS = 40_000_000  # repo arm's cpu_baseline: ~15 s of sequential ALGO-REF on config 5
+REF_STEP_DIFFUSIONS = 8_000_000     # --impl reference: ~3 s per step
 
 
 def load_peaks():
@@ -153,45 +156,61 @@ def barrier(world):
 
 
 # ------------------------------------------------------------------ CPU baseline
-def cpu_sample(seconds_cap=None):
-    """Reference algorithm (oracle port, bit-exact with fluidrank.engine.run + sweep scheduler)
-    on the config-5 generator scaled to N=1M nodes: one full solve to residual 1e-9."""
+def cpu_sample(off, tgt, damping, target, budget, graph_name):
+    """Reference algorithm (oracle port, bit-exact with fluidrank.engine.run + ThresholdSweepScheduler)
+    on the benchmarked graph itself, from the initial state for `budget` diffusions (one host core:
+    the algorithm is sequential).  Only the C solve is timed."""
     from oracle import oracle as O
     O.build()
-    w = WORKLOADS[5]
-    src, dst = O.gen_edges(O.web_config(w["mean"]), CPU_SAMPLE_N, 1)
-    off, tgt, stats = O.csr_build(CPU_SAMPLE_N, src, dst, clean=True)
-    del src, dst
-    t0 = time.perf_counter()
-    r = O.run_seq(off, tgt, w["damping"], w["target"], "sweep")
-    dt = time.perf_counter() - t0
-    return {"value": r.elementary_steps / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": (f"config-5 generator scaled to N={CPU_SAMPLE_N:,} (L={stats[0]:,}), one full solve "
-                       f"to residual 1e-9: {r.elementary_steps:,} edges in {dt:.2f} s, sequential "
-                       "ALGO-REF + ThresholdSweepScheduler (oracle/fr_oracle.c, bit-exact with the reference)"),
-            "seconds": dt, "elementary_steps": r.elementary_steps}
+    r = O.run_seq(off, tgt, damping, target, "sweep", max_diffusions=budget)
+    return {"value": r.elementary_steps / r.seconds, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": (f"{graph_name}: sequential ALGO-REF + ThresholdSweepScheduler (oracle/fr_oracle.c, "
+                       f"bit-exact with the reference) from the initial state, first {budget:,} diffusions: "
+                       f"{r.elementary_steps:,} edges in {r.seconds:.2f} s"),
+            "seconds": r.seconds, "elementary_steps": r.elementary_steps, "diffusions": r.diffusions}
+
+
+def cpu_full_solve(off, tgt, damping, target, graph_name):
+    """One complete sequential reference solve to the target (time to residual on the host)."""
+    from oracle import oracle as O
+    O.build()
+    r = O.run_seq(off, tgt, damping, target, "sweep")
+    return {"graph": graph_name, "time_to_residual_s": r.seconds, "edges": r.elementary_steps,
+            "edges_per_s": r.elementary_steps / r.seconds, "diffusions": r.diffusions,
+            "final_residual": r.residual, "cores": 1, "kind": "port",
+            "algorithm": "sequential ALGO-REF + ThresholdSweepScheduler(decay 0.5), oracle/fr_oracle.c"}
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
+    from oracle import oracle as O
+    O.build()
+    w = WORKLOADS[args.config]
+    n = args.n or w["n"]
+    t0 = time.perf_counter()
+    off, tgt, rep = O.gen_graph_exact(O.web_config(w["mean"]), n, args.seed)
+    t_graph = time.perf_counter() - t0
+    name = f"{w['name']} (exact-size graph: {tgt.size:,} edges; seed {args.seed})"
     for _ in range(args.warmup):
-        cpu_sample()
-    vals, secs, steps = [], [], 0
+        cpu_sample(off, tgt, w["damping"], w["target"], REF_STEP_DIFFUSIONS, name)
+    secs, steps = 0.0, 0
     for _ in range(args.steps):
-        s = cpu_sample()
-        vals.append(s["value"])
-        secs.append(s["seconds"])
-        steps += s["elementary_steps"]
-        last = s
-    total = sum(secs)
-    value = steps / total
+        smp = cpu_sample(off, tgt, w["damping"], w["target"], REF_STEP_DIFFUSIONS, name)
+        secs += smp["seconds"]
+        steps += smp["elementary_steps"]
+    value = steps / secs
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": last["sample"], "parallelism": "1 host core (sequential algorithm)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": last["sample"]},
+            "config": {"workload": w["name"], "n": n, "edges": int(tgt.size), "seed": args.seed,
+                       "graph": "oracle.gen_graph_exact (bit-exact with the device generator)",
+                       "graph_build_s": t_graph,
+                       "step": (f"sequential ALGO-REF + ThresholdSweepScheduler from the initial state for "
+                                f"{REF_STEP_DIFFUSIONS:,} diffusions (a bounded sample of one solve)"),
+                       "parallelism": "1 host core (sequential algorithm)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": smp["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -236,18 +255,13 @@ def run_ours(args, world, rank, local):
     n = w["n"]
     dev = torch.device("cuda", local)
     t0 = time.perf_counter()
-    cfg = gen.web_config(w["mean"])
-    src, dst = gen.generate_edges(cfg, n, args.seed)
+    # the exact-size graph: base draw, cleaned, fill rounds redrawing the dropped slots
+    g, grep_ = gen.generate(gen.web_config(w["mean"]), n, args.seed, exact=True)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    off, tgt, (L, dups, loops) = fr.csr_build(n, src, dst, clean=True)
-    torch.cuda.synchronize()
-    t_csr = time.perf_counter() - t0
-    slots = src.numel()
-    del src, dst
+    off, tgt = g.out_offsets, g.out_targets
+    L = g.edge_count
     torch.cuda.empty_cache()
-    g = fr.SparseGraph(n, off, tgt)
     fp32 = args.fluid == "fp32"
     params = fr.DiffusionParams(damping=w["damping"], target_error=w["target"])
     sched = fr.make_scheduler("sweep", policy=args.policy, sweep_decay=args.decay,
@@ -411,9 +425,25 @@ def run_ours(args, world, rank, local):
         e1.record(stream)
         torch.cuda.synchronize()
         t_pi = reduce_max(e0.elapsed_time(e1), world) / 1000.0
+        # SpMV roofline: the same iterations host-launched with events around the SpMV
+        _, it_p, spmv_ms, rest_ms = pi.run_profiled(w["target"])
+        spmv_bytes = 12 * L + 16 * n  # per iteration: 4 B index + 8 B gathered z per edge; 8 B offset + 8 B sum per row
+        rest_bytes = 48 * n           # update pass: read s, v, x, 1/deg; write x, z
+        spmv_ach = spmv_bytes / (spmv_ms / it_p / 1000.0) / 1e9
         power = {"time_s": t_pi, "iterations": iters, "edges": iters * L, "edges_per_s": iters * L / t_pi,
                  "transpose_build_s": t_tr, "rank_l1_vs_diffusion": float((x_pi - rank_out).abs().sum()),
-                 "stopping_rule": "|x_n - x_{n-1}|_1 * d/(1-d) <= 1e-9 (baseline.py:52)"}
+                 "stopping_rule": "|x_n - x_{n-1}|_1 * d/(1-d) <= 1e-9 (baseline.py:52)",
+                 "roofline": {"bound": "hbm", "kernel": "k_pi_rows + k_pi_segs (pull SpMV)",
+                              "achieved": round(spmv_ach, 1), "peak": load_peaks()[0], "unit": "GB/s",
+                              "frac": round(spmv_ach / load_peaks()[0], 4),
+                              "bytes_per_iteration": spmv_bytes, "avg_iteration_ms": spmv_ms / it_p,
+                              "update_pass_ms": rest_ms / it_p,
+                              "update_pass_frac": round(rest_bytes / (rest_ms / it_p / 1000.0) / 1e9
+                                                        / load_peaks()[0], 4),
+                              "algorithmic_bytes_definition": "12 B per edge (4 B source index + 8 B gathered "
+                                                              "x/deg) + 16 B per row (offset, sum)",
+                              "timing": "host-launched iterations, CUDA events around the SpMV kernels"},
+                 "vs_diffusion_time": t_pi / (ms_per_step / 1000.0)}
         pi.close()
         del x_pi
         g._reverse = None
@@ -449,10 +479,13 @@ def run_ours(args, world, rank, local):
     # ---- the other single-solve BASELINE configs (1: N=10k uniform, 2: N=1M web,
     # 3: N=20M web in fp64 and fp32 fluid), same schedule, graph resident
     others = None
+    c3_host = None  # host CSR of config 3 for the CPU reference solve
     if not args.no_configs:
         others = {}
         for k in (1, 2, 3):
             gk, rk = gen.baseline_graph(k, seed=args.seed)
+            if k == 3 and not args.no_cpu_c3 and rank == 0:
+                c3_host = (gk.out_offsets.cpu().numpy(), gk.out_targets.cpu().numpy().view(np.uint32))
             pk = fr.DiffusionParams(damping=0.85, target_error=gen.CONFIGS[k]["target_error"])
             leg = {"n": gk.n, "edges": gk.edge_count, "target_error": pk.target_error}
             ranks = {}
@@ -500,9 +533,27 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         t4 = reduce_max(e0.elapsed_time(e1), world) / 1000.0
         colsum = float((rank4.sum(0) - 1.0).abs().max())
-        ppr = {"workload": "BASELINE configs[3]: N=1M web graph (mean out-degree 8, %d edges), 64 vectors x 10 "
+        peak = load_peaks()[0]
+        # algorithmic bytes: every sweep scans the n x B fluid rows (8 B x B each); a row visit
+        # takes the row (8 B x B) and adds it to the history (16 B x B); an edge visit reads its
+        # 4 B column index and scatters one 8 B red.add per non-zero column value (pushes)
+        Bc = 64
+        ppr_bytes = (st4.sweeps * g4.n * 8 * Bc + st4.diffusions * 24 * Bc + st4.elementary_steps * 4
+                     + st4.hub_edges * 8)
+        ppr_ach = ppr_bytes / t4 / 1e9
+        ppr_roof = {"bound": "hbm", "achieved": round(ppr_ach, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(ppr_ach / peak, 4), "column_pushes": st4.hub_edges,
+                    "pushes_per_s": st4.hub_edges / t4,
+                    "l2_atomic_envelope_per_s": {"l2_resident": 2.0e11, "local_window_streamed": 8.0e10,
+                                                 "uniform_800MB": 2.3e10, "source": "tools/red_probe.cu (DESIGN.md)"},
+                    "algorithmic_bytes_definition": "8 B x 64 per row per sweep (scan) + 24 B x 64 per row visit "
+                                                    "(take, history r/w) + 4 B per edge visit + 8 B per pushed "
+                                                    "column value",
+                    "timing": "whole solve, CUDA events (k_ppr_sweep dominates)"}
+        ppr = {"roofline": ppr_roof,"workload": "BASELINE configs[3]: N=1M web graph (mean out-degree 8, %d edges), 64 vectors x 10 "
                            "seeds, d=0.85, each column to L1 residual 1e-9, n x 64 fp64 row-major state" % g4.edge_count,
                "time_s": t4, "sweeps": st4.sweeps, "row_visits": st4.diffusions, "edge_visits": st4.elementary_steps,
+               "column_pushes": st4.hub_edges,
                "max_column_residual": max(res4), "max_column_sum_error": colsum, "decay": 0.6,
                "timing": "one fr_ppr_init + fr_ppr_run + normalize, CUDA events"}
         pp.close()
@@ -540,13 +591,26 @@ def run_ours(args, world, rank, local):
 
     line = None
     if rank == 0:
-        cpu = cpu_sample() if not args.no_cpu else None
+        cpu = None
+        if not args.no_cpu:
+            # the reference algorithm on the benchmarked graph itself (host copy of the device CSR)
+            cpu = cpu_sample(h_off.numpy(), h_tgt.numpy().view(np.uint32), w["damping"], w["target"],
+                             CPU_SAMPLE_DIFFUSIONS, f"{w['name']} (this run's graph, {L:,} edges)")
+        cpu_c3 = None
+        if c3_host is not None:
+            cpu_c3 = cpu_full_solve(c3_host[0], c3_host[1], 0.85, gen.CONFIGS[3]["target_error"],
+                                    "config3: N=20M web graph, mean out-degree 10 (the other_configs.config3 graph)")
+            if others:
+                cpu_c3["gpu_speedup_time_to_residual"] = (cpu_c3["time_to_residual_s"]
+                                                           / others["config3"]["fp64"]["time_to_residual_s"])
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32-fluid/f64-history" if fp32 else "f64", "data": "synthetic",
-            "config": {"workload": w["name"], "n": n, "edges": L, "edge_slots_drawn": slots,
-                       "duplicates_dropped": dups, "self_loops_dropped": loops, "damping": w["damping"],
+            "config": {"workload": w["name"], "n": n, "edges": L, "edges_configured": grep_.target_links,
+                       "edges_unfilled": grep_.unfilled, "fill_rounds": grep_.rounds,
+                       "edge_slots_drawn": grep_.slots, "duplicates_dropped": grep_.duplicates,
+                       "self_loops_dropped": grep_.self_loops, "damping": w["damping"],
                        "target_error": w["target"], "policy": args.policy, "decay": args.decay,
                        "edge_frac": args.edge_frac if args.policy == "adaptive" else None,
                        "kernel_path": args.path, "hot_slots": args.hot_slots, "warm_slots": args.warm_slots,
@@ -556,7 +620,10 @@ def run_ours(args, world, rank, local):
             "time_to_residual_s": ms_per_step / 1000.0,
             "sweeps_per_solve": last.sweeps, "diffusions_per_solve": last.diffusions,
             "edges_per_solve": last.elementary_steps, "final_residual": last.residual,
-            "graph_gen_s": t_gen, "csr_build_s": t_csr,
+            "graph_build_s": t_gen,
+            "solver_setup": ("fr_solver_create (slot classes from a sampled in-degree, encoded column copy, "
+                             "narrow offsets) runs once before the timed solves: the graph stays resident and "
+                             "is solved many times; e2e includes it on every call"),
             "e2e": {"value": e2e_edges / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": 8 * (n + 1) + 4 * L, "d2h_bytes_per_step": 8 * n,
                     "seconds_per_step": e2e_s / e2e_steps, "steps": e2e_steps,
@@ -569,6 +636,7 @@ def run_ours(args, world, rank, local):
             "ppr": ppr, "other_configs": others,
             "roofline": roofline,
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_config3_full_solve": cpu_c3,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -601,6 +669,7 @@ def main():
     ap.add_argument("--block-min", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-c3", action="store_true", help="skip the full sequential CPU solve of config 3")
     ap.add_argument("--no-d099", action="store_true", help="skip the d=0.99 solve")
     ap.add_argument("--no-ppr", action="store_true", help="skip the batched PPR (configs[3]) solve")
     ap.add_argument("--no-plain", action="store_true", help="skip the beta=0 comparison solve")

@@ -233,6 +233,11 @@ int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offsets, const in
 /* x <- teleport, iterate until |x_n - x_{n-1}|_1 * d/(1-d) <= target_error. */
 int fr_power_run(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
                  int64_t *h_iterations, double *h_diff, void *stream);
+/* Same iterations launched from the host with CUDA events (roofline report, not
+ * the timed path): h_ms[0] = SpMV time (row tiles + long-row segments), h_ms[1] =
+ * the rest (dangling mass, update, check), summed over the iterations. */
+int fr_power_run_profiled(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
+                          int64_t *h_iterations, double *h_ms, void *stream);
 int fr_power_destroy(fr_power *p);
 
 /* ------------------------------------------------------------------ */
@@ -249,7 +254,9 @@ int fr_ppr_init(int64_t n, int32_t B, const uint32_t *d_seeds, int32_t k, double
 /* cfg: damping, target_error, decay (geometric theta), max_sweeps. */
 int fr_ppr_create(int64_t n, int64_t m, const int64_t *d_offsets, const uint32_t *d_targets, int32_t B,
                   double *d_fluid, double *d_history, const fr_solver_config *cfg, void *stream, fr_ppr **out);
-/* h_col_residual (B): exact final residual of each column. */
+/* h_col_residual (B): exact final residual of each column.  h_stats:
+ * diffusions = row visits, elementary_steps = edge visits, hub_edges = column
+ * values scattered (one red.add each; zero pushes are skipped). */
 int fr_ppr_run(fr_ppr *p, void *stream, fr_solve_stats *h_stats, double *h_col_residual);
 int fr_ppr_destroy(fr_ppr *p);
 /* rank[:, c] = history[:, c] / sum |history[:, c]|. */

@@ -143,6 +143,21 @@ void fro_gen_zipf_table(int64_t n, double s, double *cdf)
     cdf[n - 1] = 1.0;
 }
 
+/* The Zipf table of the last (n, s) asked for, kept across fill rounds. */
+static double *zipf_cache;
+static int64_t zipf_cache_n = -1;
+static double zipf_cache_s;
+static const double *zipf_cached(int64_t n, double s)
+{
+    if (zipf_cache && zipf_cache_n == n && zipf_cache_s == s) return zipf_cache;
+    free(zipf_cache);
+    zipf_cache = (double *)malloc(sizeof(double) * (size_t)n);
+    zipf_cache_n = zipf_cache ? n : -1;
+    zipf_cache_s = s;
+    if (zipf_cache) fro_gen_zipf_table(n, s, zipf_cache);
+    return zipf_cache;
+}
+
 /* Keyed Feistel bijection on [0, n) with cycle walking: the "random
  * permutation of node IDs" the Zipf targets are drawn over. */
 static uint64_t feistel(uint64_t x, uint64_t n, const uint64_t keys[4], int half)
@@ -179,6 +194,7 @@ int64_t fro_gen_degrees(const fro_gen_config *c, int64_t n, uint64_t seed, uint3
     uint64_t kd = stream_key(seed, FRO_STREAM_DEG);
     int64_t total = 0;
     if (c->kind == 0) {
+#pragma omp parallel for reduction(+ : total) schedule(static)
         for (int64_t u = 0; u < n; u++) {
             uint64_t g = frand(kd, (uint64_t)u, 0) % (uint64_t)(c->max_out + 1);
             if (n < 2) g = 0;
@@ -192,6 +208,7 @@ int64_t fro_gen_degrees(const fro_gen_config *c, int64_t n, uint64_t seed, uint3
     uint64_t scale_q32;
     if (!cdf || fro_gen_powerlaw_table(c, cdf, &scale_q32)) { free(cdf); return -1; }
     uint32_t dthr = frac_to_u32(c->dangling_frac);
+#pragma omp parallel for reduction(+ : total) schedule(static)
     for (int64_t u = 0; u < n; u++) {
         uint64_t g = 0;
         if (n >= 2 && (uint32_t)(frand(kd, (uint64_t)u, 0) >> 32) >= dthr) {
@@ -284,24 +301,27 @@ int fro_gen_edges_round(const fro_gen_config *c, int64_t n, uint64_t seed, uint3
     uint64_t fk[4];
     for (int r = 0; r < 4; r++) fk[r] = stream_key(seed, FRO_STREAM_FEISTEL + r);
     int half = feistel_half((uint64_t)n);
-    double *zcdf = NULL;
-    if (c->kind == 1) {
-        zcdf = (double *)malloc(sizeof(double) * (size_t)n);
-        if (!zcdf) return -1;
-        fro_gen_zipf_table(n, c->zipf_s, zcdf);
-    }
+    const double *zcdf = NULL;
+    if (c->kind == 1 && !(zcdf = zipf_cached(n, c->zipf_s))) return -1;
     uint32_t lthr = frac_to_u32(c->local_frac);
-    int64_t e = 0;
+    int64_t *eoff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    if (!eoff) return -1;
+    eoff[0] = 0;
+    for (int64_t u = 0; u < n; u++) eoff[u + 1] = eoff[u] + deg[u];
     const int64_t wfull = 2 * (int64_t)c->window < n - 1 ? 2 * (int64_t)c->window : n - 1;
+    /* every slot is a pure function of (seed, round, u, j): the order of the
+     * per-node work does not change the output */
+#pragma omp parallel for schedule(dynamic, 4096)
     for (int64_t u = 0; u < n; u++) {
         if (!deg[u]) continue;
         const int zonly = c->kind == 1 && off && window_count(tgt, off[u], off[u + 1], u, c->window, n) >= wfull;
+        int64_t e = eoff[u];
         for (int64_t j = 0; j < (int64_t)deg[u]; j++, e++) {
             src[e] = (uint32_t)u;
             dst[e] = gen_target(c, n, ke, kz, zcdf, fk, half, lthr, u, j, zonly);
         }
     }
-    free(zcdf);
+    free(eoff);
     return 0;
 }
 
@@ -348,10 +368,12 @@ int fro_csr_build(int64_t n, int64_t m, const uint32_t *src, const uint32_t *dst
     for (int64_t e = 0; e < m; e++)
         if (src[e] != dst[e]) tgt[cur[src[e]]++] = dst[e];
     free(cur);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t i = 0; i < n; i++)
+        qsort(tgt + off[i], (size_t)(off[i + 1] - off[i]), sizeof(uint32_t), cmp_u32);
     int64_t w = 0;
     for (int64_t i = 0; i < n; i++) {
         int64_t b = off[i], e = off[i + 1];
-        qsort(tgt + b, (size_t)(e - b), sizeof(uint32_t), cmp_u32);
         off[i] = w;
         for (int64_t k = b; k < e; k++) {
             if (k > b && tgt[k] == tgt[k - 1]) {
@@ -389,23 +411,39 @@ int fro_csr_merge(int64_t n, const int64_t *off, const uint32_t *tgt, int64_t m2
     memcpy(cur, o2, sizeof(int64_t) * (size_t)n);
     for (int64_t e = 0; e < m2; e++)
         if (src2[e] != dst2[e]) t2[cur[src2[e]]++] = dst2[e];
-    int64_t w = 0;
+    /* pass 1 (rows in parallel): sort the extra edges, size of each row's union */
+#pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < n; i++) {
         int64_t b2 = o2[i], e2 = o2[i + 1];
+        if (e2 == b2) { cur[i] = off[i + 1] - off[i]; continue; }
         qsort(t2 + b2, (size_t)(e2 - b2), sizeof(uint32_t), cmp_u32);
-        int64_t a = off[i], ae = off[i + 1], k = b2;
-        off_out[i] = w;
-        int64_t row0 = w;
+        int64_t a = off[i], ae = off[i + 1], k = b2, cnt = 0;
+        uint32_t last = 0;
         while (a < ae || k < e2) {
             const uint32_t v = (k >= e2 || (a < ae && tgt[a] <= t2[k])) ? tgt[a++] : t2[k++];
-            if (w > row0 && tgt_out[w - 1] == v) {  /* the existing row is unique: a repeat is an extra edge */
-                dups++;
-                continue;
-            }
-            tgt_out[w++] = v;
+            if (cnt && last == v) continue;
+            last = v;
+            cnt++;
         }
+        cur[i] = cnt;
+    }
+    int64_t w = 0;
+    for (int64_t i = 0; i < n; i++) {
+        off_out[i] = w;
+        w += cur[i];
     }
     off_out[n] = w;
+    dups = (off[n] + (m2 - loops)) - w;  /* the existing rows are unique: every repeat is an extra edge */
+    /* pass 2 (rows in parallel): write the unions */
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t i = 0; i < n; i++) {
+        int64_t a = off[i], ae = off[i + 1], k = o2[i], e2 = o2[i + 1], o = off_out[i], row0 = o;
+        while (a < ae || k < e2) {
+            const uint32_t v = (k >= e2 || (a < ae && tgt[a] <= t2[k])) ? tgt[a++] : t2[k++];
+            if (o > row0 && tgt_out[o - 1] == v) continue;
+            tgt_out[o++] = v;
+        }
+    }
     free(o2); free(t2); free(cur);
     if (stats) { stats[0] = w; stats[1] = dups; stats[2] = loops; }
     return 0;

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -239,6 +240,7 @@ class OracleRun:
     elementary_steps: int
     sweeps: int
     trace: np.ndarray  # rows (elementary_steps, diffusions, residual, bound)
+    seconds: float = 0.0  # the C solve alone (fro_run_seq), wall clock
 
 
 def _trace_array(rows, length):
@@ -262,19 +264,21 @@ def run_seq(off, tgt, damping=0.85, target_error=1e-8, kind="sweep", decay=0.5,
     signed = bool(np.any(fluid < 0.0))
     if residual is None:
         residual = pairwise_sum(fluid, absval=signed)
-    in_deg = in_degree(n, tgt)
+    in_deg = in_degree(n, tgt) if kind == "op" else None  # only the op weights read it
     rows = (TraceRow * trace_cap)()
     rank = np.empty(n)
     res = RunResult()
+    t0 = time.perf_counter()
     rc = lib().fro_run_seq(n, _ptr(off), _ptr(tgt), _ptr(in_deg), damping, target_error,
                            KIND_CODES[kind], decay, -1 if max_diffusions is None else max_diffusions,
                            0 if trace_every is None else trace_every, int(signed), _ptr(fluid),
                            _ptr(history), residual, 0, 0, rows, trace_cap, _ptr(rank),
                            ctypes.byref(res))
+    elapsed = time.perf_counter() - t0
     if rc == 3:
         raise RuntimeError("scheduler starved")
     return OracleRun(rank, history, fluid, res.residual, res.diffusions, res.elementary_steps,
-                     0, _trace_array(rows, res.trace_len))
+                     0, _trace_array(rows, res.trace_len), elapsed)
 
 
 def run_psweep(off, tgt, damping=0.85, target_error=1e-8, policy=0, decay=0.5,

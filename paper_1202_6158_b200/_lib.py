@@ -85,6 +85,7 @@ SIGNATURES = {
     "fr_solver_destroy": (ctypes.c_int, [_P]),
     "fr_power_create": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _F64, _P, _P, _P]),
     "fr_power_run": (ctypes.c_int, [_P, _F64, _I64, _P, _P, _P, _P]),
+    "fr_power_run_profiled": (ctypes.c_int, [_P, _F64, _I64, _P, _P, _P, _P]),
     "fr_power_destroy": (ctypes.c_int, [_P]),
     "fr_pagerank_host": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _P, _P]),
     "fr_ppr_init": (ctypes.c_int, [_I64, _I32, _P, _I32, _F64, _P, _P, _P]),

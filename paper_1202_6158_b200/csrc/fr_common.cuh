@@ -164,6 +164,19 @@ __device__ __forceinline__ void red_add(float *p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// Fire-and-forget global add with an L2 cache-policy hint (createpolicy).
+__device__ __forceinline__ void red_add_hint(double *p, double v, u64 pol) {
+    asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void red_add_hint(float *p, float v, u64 pol) {
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ u64 policy_evict_first() {
+    u64 pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 // Streaming (read-once) loads that do not allocate in L1.
 __device__ __forceinline__ uint4 ld_stream_u4(const uint4 *p) {
     uint4 r;

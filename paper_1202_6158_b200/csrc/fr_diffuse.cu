@@ -573,6 +573,12 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #ifndef FR_OWN_UNROLL
 #define FR_OWN_UNROLL 3  // column loads in flight per lane and batch (k_sweep: FR_SW_UNROLL)
 #endif
+#ifndef FR_COLD_HINT
+#define FR_COLD_HINT 0
+#endif
+#ifndef FR_OWN_SKIPSCAN
+#define FR_OWN_SKIPSCAN 0
+#endif
 static constexpr int OWN_NT = FR_OWN_NT;
 static constexpr int OWN_UNROLL = FR_OWN_UNROLL;
 static_assert(OWN_UNROLL * 6 <= 32, "packed row indices");
@@ -611,6 +617,9 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
     const IT nn = (IT)a.n;
     const u32 *__restrict__ tgt = a.tgt;
     FT *__restrict__ F = a.F;
+#if FR_COLD_HINT
+    const u64 cold_pol = policy_evict_first();
+#endif
     for (u32 q = threadIdx.x; q < CH; q += OWN_NT) acc[q] = (FT)0;
     hot_clear(hot_acc, a.nhot, OWN_NT);
     for (int q = threadIdx.x; q < DSC_TAB; q += OWN_NT) dsc_sm[q] = q ? a.d / (double)q : 0.0;
@@ -696,6 +705,17 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
             }
             const u32 adeg = act ? deg : 0u;
             u32 incl = adeg;
+#if FR_OWN_SKIPSCAN
+            // a tile with nothing to push skips the scan (sparse sweeps)
+            const u32 total = __reduce_add_sync(FULL, adeg);
+            if (total)
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 t = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += t;
+                }
+            const u32 start = incl - adeg;
+#else
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const u32 t = __shfl_up_sync(FULL, incl, o);
@@ -703,6 +723,7 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
             }
             const u32 start = incl - adeg;
             const u32 total = __shfl_sync(FULL, incl, 31);
+#endif
             // column batches: the targets in registers, each lane's row (r + 1, 0 = past
             // the end) packed 6 bits per batch slot into one register
             u32 tvA[OWN_UNROLL], tvB[OWN_UNROLL], tvC[OWN_UNROLL];
@@ -767,6 +788,10 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                         const u32 t = tv[u];
                         const u32 lt2 = t - ubase;
                         if (!(slotted && (t & HOT_FLAG)) && lt2 < len) atomicAdd(acc + lt2, v);  // inside the chunk
+#if FR_COLD_HINT
+                        else if (!(slotted && (t & HOT_FLAG)) && (t - ubase + 4096u) > CH + 8192u)
+                            red_add_hint(F + t, v, cold_pol);  // far, unslotted: do not displace the front
+#endif
                         else push_one(F, a.Fw, hot_acc, a.nhot, t, v, slotted);
                     }
                 }

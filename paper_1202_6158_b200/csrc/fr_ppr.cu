@@ -26,6 +26,7 @@ struct PprCtl {
     u64 active;            // bit c: column c still diffusing
     u64 need_check;        // columns whose incremental residual crossed the target
     u64 diffusions, steps, sweeps;
+    u64 pushes;            // column values scattered (one red.add each)
     u64 seg_next[PP_SEGS];
     u32 stop;
     u32 pad;
@@ -38,7 +39,7 @@ struct PprArgs {
     PprCtl *ctl;
     double *part_abs;    // [grid][64]
     double *part_max;    // [grid]
-    u64 *part_sel, *part_steps;
+    u64 *part_sel, *part_steps, *part_push;
     double *part_mass;   // [grid][64] for exact checks
     long long n;
     int B;
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
     const bool own0 = lane < B && ((active >> lane) & 1ull);
     const bool own1 = lane + 32 < B && ((active >> (lane + 32)) & 1ull);
     double ab0 = 0.0, ab1 = 0.0, mx = 0.0;
-    u64 nsel = 0, steps = 0;
+    u64 nsel = 0, steps = 0, npush = 0;
     const long long seg_len = (a.n + PP_SEGS - 1) / PP_SEGS;
     int seg = (int)((blockIdx.x * (PP_NT / 32) + wid) % PP_SEGS), misses = 0;
     long long node = 0, chunk_end = 0;
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
                 if (lane == 0) steps += deg;
                 const double w = a.d / (double)deg;
                 const double p0 = s0 * w, p1 = s1 * w;  // sent*(d/deg), engine.py:321
+                npush += (u64)deg * ((own0 && p0 != 0.0) + (own1 && p1 != 0.0));
                 for (u32 k0 = 0; k0 < deg; k0 += 32) {
                     const u32 cnt = deg - k0 < 32u ? deg - k0 : 32u;
                     const u32 tv = lane < cnt ? __ldg(a.tgt + lo + k0 + lane) : 0u;
@@ -146,10 +148,12 @@ __global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
     const double bmx = block_max<PP_NT>(mx, s_red);
     const u64 bsel = block_sum_u64<PP_NT>(nsel, s_red64);
     const u64 bst = block_sum_u64<PP_NT>(steps, s_red64);
+    const u64 bpu = block_sum_u64<PP_NT>(npush, s_red64);
     if (threadIdx.x == 0) {
         a.part_max[blockIdx.x] = bmx;
         a.part_sel[blockIdx.x] = bsel;
         a.part_steps[blockIdx.x] = bst;
+        a.part_push[blockIdx.x] = bpu;
     }
 }
 
@@ -223,12 +227,14 @@ __global__ void k_ppr_finalize(PprArgs a) {
     if (col == 0) {
         s_need = 0;
         double mx = 0.0;
-        u64 sel = 0, st = 0;
+        u64 sel = 0, st = 0, pu = 0;
         for (int p = 0; p < a.nparts; p++) {
             mx = fmax(mx, a.part_max[p]);
             sel += a.part_sel[p];
             st += a.part_steps[p];
+            pu += a.part_push[p];
         }
+        c->pushes += pu;
         s_max = mx;
         c->diffusions += sel;
         c->steps += st;
@@ -379,7 +385,7 @@ extern "C" int fr_ppr_create(int64_t n, int64_t m, const int64_t *d_offsets, con
         cudaError_t e;
         if ((e = cudaMalloc(&p->ctl, sizeof(PprCtl))) != cudaSuccess ||
             (e = cudaMalloc(&p->parts, sizeof(double) * (size_t)p->grid * (64 + 1 + 64))) != cudaSuccess ||
-            (e = cudaMalloc(&p->parts64, sizeof(u64) * (size_t)p->grid * 2)) != cudaSuccess) {
+            (e = cudaMalloc(&p->parts64, sizeof(u64) * (size_t)p->grid * 3)) != cudaSuccess) {
             rc = cuda_fail(e, "cudaMalloc(ppr)", __FILE__, __LINE__);
             break;
         }
@@ -394,6 +400,7 @@ extern "C" int fr_ppr_create(int64_t n, int64_t m, const int64_t *d_offsets, con
         a.part_mass = p->parts + (size_t)p->grid * 65;
         a.part_sel = p->parts64;
         a.part_steps = p->parts64 + p->grid;
+        a.part_push = p->parts64 + 2 * (size_t)p->grid;
         a.n = n;
         a.B = B;
         a.nparts = p->grid;
@@ -462,7 +469,7 @@ extern "C" int fr_ppr_run(fr_ppr *p, void *stream, fr_solve_stats *h_stats, doub
         h_stats->residual = mx;
         h_stats->theta = c.theta;
         h_stats->trace_len = 0;
-        h_stats->hub_edges = 0;
+        h_stats->hub_edges = (int64_t)c.pushes;  // batched PPR: column values scattered
     }
     if (h_col_residual)
         for (int col = 0; col < p->B; col++) h_col_residual[col] = c.exact[col];

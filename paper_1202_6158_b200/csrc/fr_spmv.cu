@@ -5,8 +5,9 @@
 // over the transposed CSR (rows = targets, columns = sources ascending, the
 // reference's graph.to_matrix(), graph.py:158-165):
 //   s_i = sum_{j in in(i)} z_j,   z_j = x_j / outdeg_j (0 for dangling j)
-// Short rows: one 8-lane group per row.  Rows longer than LONG_ROW are split
-// into warp-sized segments whose partial sums are combined with atomics.
+// Short rows: warp per tile of 32 rows over the tile's compacted edge space
+// (k_pi_rows).  Rows longer than LONG_ROW are split into warp-sized segments
+// whose partial sums are combined with atomics.
 // The iteration loop is a CUDA-graph while-node (no host round trip).
 #include <math.h>
 
@@ -60,31 +61,104 @@ __global__ void __launch_bounds__(PI_NT) k_pi_init(PiArgs a) {
     }
 }
 
-// 8 lanes per row; long rows only get their accumulator cleared here.
+// Warp per tile of 32 consecutive rows; rows longer than LONG_ROW are left at 0
+// here (their warp segments add into them in k_pi_segs).  The tile's short rows
+// are contiguous ranges of in_src, so their concatenation (the tile's compacted
+// edge space, E edges) is split into 32 equal contiguous chunks, one per lane:
+// every lane streams its column indices in order with PI_UNROLL independent
+// loads and gathers in flight, and adds its partial sum of a row to the row's
+// shared-memory accumulator when it walks past the row's end.  Per-lane work is
+// E/32 edges whatever the degree mix, and the 32-row tiles of a grid-stride
+// round are adjacent, so the gathered window of z stays in L2.
+static constexpr int PI_UNROLL = 4;
 __global__ void __launch_bounds__(PI_NT) k_pi_rows(PiArgs a) {
-    __shared__ double sm[PI_NT / 32];
-    const int sub = threadIdx.x & 7;
-    const long long groups = (long long)gridDim.x * (PI_NT / 8);
+    constexpr u32 FULL = 0xffffffffu;
+    constexpr int NW = PI_NT / 32;
+    __shared__ u32 s_pre[NW][33];
+    __shared__ u64 s_lo[NW][32];
+    __shared__ double s_acc[NW][32];
+    __shared__ double sm[NW];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long ntiles = (a.n + 31) / 32;
+    const long long nwarps = (long long)gridDim.x * NW;
     double acc_block = 0.0;
-    const long long g0 = blockIdx.x * (long long)(PI_NT / 8) + (threadIdx.x >> 3);
-    // uniform trip count so the 8-lane shuffles stay converged
-    const long long trips = (a.n + groups - 1) / groups;
-    for (long long t = 0; t < trips; t++) {
-        const long long i = g0 + t * groups;
-        double acc = 0.0;
-        bool long_row = false;
-        if (i < a.n) {
-            const u64 lo = a.in_off[i], hi = a.in_off[i + 1];
-            long_row = hi - lo > LONG_ROW;
-            if (!long_row)
-                for (u64 k = lo + sub; k < hi; k += 8) acc += a.z[__ldg(a.in_src + k)];
+    for (long long t = blockIdx.x * (long long)NW + w; t < ntiles; t += nwarps) {
+        const long long r = t * 32 + lane;
+        u64 lo = 0, deg = 0;
+        if (r < a.n) {
+            lo = a.in_off[r];
+            deg = a.in_off[r + 1] - lo;
+            if (deg > LONG_ROW) deg = 0;
         }
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        if (i < a.n && sub == 0) {
-            a.s[i] = acc;  // 0 for long rows: their segments accumulate next
-            acc_block += acc;
+        u32 inc = (u32)deg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const u32 E = __shfl_sync(FULL, inc, 31);
+        __syncwarp();
+        s_pre[w][lane + 1] = inc;
+        if (lane == 0) s_pre[w][0] = 0;
+        s_lo[w][lane] = lo;
+        s_acc[w][lane] = 0.0;
+        __syncwarp();
+        const u32 chunk = (E + 31) >> 5;
+        u32 q = lane * chunk;
+        const u32 qe = min(E, q + chunk);
+        if (q < qe) {
+            // the row holding edge q: the largest k with pre[k] <= q
+            int k = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1)
+                if (s_pre[w][k + step] <= q) k += step;
+            u32 rend = s_pre[w][k + 1];
+            u64 base = s_lo[w][k] - s_pre[w][k];  // in_src position of edge q' of row k: base + q'
+            double acc = 0.0;
+            while (q < qe) {
+                u32 src[PI_UNROLL];
+                double zv[PI_UNROLL];
+                {
+                    int kk = k;
+                    u32 re = rend;
+                    u64 bs = base;
+#pragma unroll
+                    for (int j = 0; j < PI_UNROLL; j++) {
+                        src[j] = 0;
+                        if (q + j < qe) {
+                            while (q + j >= re) {
+                                kk++;
+                                re = s_pre[w][kk + 1];
+                                bs = s_lo[w][kk] - s_pre[w][kk];
+                            }
+                            src[j] = __ldg(a.in_src + bs + q + j);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < PI_UNROLL; j++) zv[j] = q + j < qe ? a.z[src[j]] : 0.0;
+#pragma unroll
+                for (int j = 0; j < PI_UNROLL; j++) {
+                    if (q < qe) {
+                        while (q >= rend) {  // left row k: hand its partial sum over
+                            if (acc != 0.0) atomicAdd(&s_acc[w][k], acc);
+                            acc = 0.0;
+                            k++;
+                            rend = s_pre[w][k + 1];
+                            base = s_lo[w][k] - s_pre[w][k];
+                        }
+                        acc += zv[j];
+                        q++;
+                    }
+                }
+            }
+            if (acc != 0.0) atomicAdd(&s_acc[w][k], acc);
+        }
+        __syncwarp();
+        if (r < a.n) {
+            const double v = s_acc[w][lane];
+            a.s[r] = v;  // 0 for long rows: their segments accumulate next
+            acc_block += v;
         }
     }
     acc_block = block_sum<PI_NT>(acc_block, sm);
@@ -351,6 +425,52 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
         return rc;
     }
     *out = p;
+    return FR_OK;
+}
+
+// The same iterations launched one by one from the host with CUDA events around
+// the SpMV (k_pi_rows + k_pi_segs) and the rest (mass, update, check): the
+// roofline report of bench.py, not the timed path.  h_ms[0] / h_ms[1] = summed
+// device time of the two classes.
+extern "C" int fr_power_run_profiled(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
+                                     int64_t *h_iterations, double *h_ms, void *stream) {
+    if (!p || !(target_error > 0.0) || !d_x || !h_ms) {
+        set_error("fr_power_run_profiled: bad arguments");
+        return FR_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    PiArgs a = p->a;
+    a.in_graph = 0;
+    a.target = target_error;
+    a.max_iter = max_iterations > 0 ? max_iterations : 1000000;
+    cudaEvent_t ev[3];
+    for (int i = 0; i < 3; i++) FR_CUDA(cudaEventCreate(&ev[i]));
+    h_ms[0] = h_ms[1] = 0.0;
+    k_pi_init<<<p->grid, PI_NT, 0, st>>>(a);
+    PiCtl hc = {};
+    for (;;) {
+        FR_CUDA(cudaEventRecord(ev[0], st));
+        k_pi_rows<<<p->grid, PI_NT, 0, st>>>(a);
+        k_pi_segs<<<p->grid, PI_NT, 0, st>>>(a);
+        FR_CUDA(cudaEventRecord(ev[1], st));
+        k_pi_mass<<<1, PI_NT, 0, st>>>(a);
+        k_pi_update<<<p->grid, PI_NT, 0, st>>>(a);
+        k_pi_check<<<1, PI_NT, 0, st>>>(a);
+        FR_CUDA(cudaEventRecord(ev[2], st));
+        FR_CUDA(cudaGetLastError());
+        FR_CUDA(cudaMemcpyAsync(&hc, p->ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
+        FR_CUDA(cudaStreamSynchronize(st));
+        float t0 = 0.f, t1 = 0.f;
+        FR_CUDA(cudaEventElapsedTime(&t0, ev[0], ev[1]));
+        FR_CUDA(cudaEventElapsedTime(&t1, ev[1], ev[2]));
+        h_ms[0] += t0;
+        h_ms[1] += t1;
+        if (hc.stop) break;
+    }
+    for (int i = 0; i < 3; i++) cudaEventDestroy(ev[i]);
+    FR_CUDA(cudaMemcpyAsync(d_x, p->a.x, sizeof(double) * (size_t)p->n, cudaMemcpyDeviceToDevice, st));
+    FR_CUDA(cudaStreamSynchronize(st));
+    if (h_iterations) *h_iterations = (int64_t)hc.iters;
     return FR_OK;
 }
 

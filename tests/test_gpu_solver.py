@@ -119,6 +119,29 @@ def test_power_iteration_long_rows(cuda, oracle):
     assert l1(rank, ox) <= 2e-9
 
 
+def test_power_iteration_row_tiles(cuda, oracle):
+    """The row-tile SpMV at its edges: in-degrees exactly at and just above the long-row
+    split (1024 / 1025), a row with every other node as parent, tiles without edges, and
+    n not a multiple of the 32-row tile."""
+    rng = np.random.default_rng(4)
+    n = 5003
+    src, dst = [], []
+    for t, k in ((0, n - 1), (1, 1024), (2, 1025), (3, 31)):
+        par = rng.choice(np.setdiff1d(np.arange(n), [t]), size=k, replace=False)
+        src.extend(par.tolist())
+        dst.extend([t] * k)
+    extra = rng.integers(64, n, (2, 3000))  # nodes 4..63 receive nothing: edge-free tiles
+    keep = extra[0] != extra[1]
+    src.extend(extra[0][keep].tolist())
+    dst.extend(extra[1][keep].tolist())
+    off, tgt, _ = oracle.csr_build(n, np.array(src, dtype=np.uint32), np.array(dst, dtype=np.uint32), clean=True)
+    g = graph_from(cuda, off, tgt)
+    x, trace = cuda.power_iterate(g, cuda.DiffusionParams(target_error=1e-12))
+    ox, iters, _ = oracle.power_iterate(off, tgt, 0.85, 1e-12)
+    assert l1(x, ox) <= 1e-13
+    assert abs(trace.rows[-1].diffusions - iters) <= 1
+
+
 def test_single_node_diffuse_bit_exact(cuda, golden_small, oracle):
     """engine.diffuse on the device equals the reference step (distinct targets: no reordering)."""
     tag = "rg3"

@@ -30,7 +30,7 @@ ap.add_argument("--warm-slots", type=int, default=0)
 ap.add_argument("variants", nargs="+")
 args = ap.parse_args()
 
-g, _ = gen.generate(gen.web_config(args.mean), args.n, 0)
+g, _ = gen.generate(gen.web_config(args.mean), args.n, 0, exact=True)
 fp32 = args.fluid == "fp32"
 params = fr.DiffusionParams(damping=args.damping, target_error=1e-9)
 first = None
