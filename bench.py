@@ -44,8 +44,8 @@ WORKLOADS = {
     2: dict(n=1_000_000, mean=8.0, damping=0.85, target=1e-9,
             name="config2: web graph N=1M, mean out-degree 8, d=0.85, fp64, L1 residual 1e-9"),
 }
-CPU_SAMPLE_DIFFUSIONS = 40_000_000  # repo arm's cpu_baseline: ~15 s of sequential ALGO-REF on config 5
-REF_STEP_DIFFUSIONS = 8_000_000     # --impl reference: ~3 s per step
+CPU_SAMPLE_DIFFUSIONS = 250_000_000  # repo arm's cpu_baseline: ~15 s of sequential ALGO-REF on config 5
+REF_STEP_DIFFUSIONS = 40_000_000     # --impl reference: ~2.5 s per step
 
 
 def load_peaks():
@@ -426,7 +426,8 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         t_pi = reduce_max(e0.elapsed_time(e1), world) / 1000.0
         # SpMV roofline: the same iterations host-launched with events around the SpMV
-        _, it_p, spmv_ms, rest_ms = pi.run_profiled(w["target"])
+        _, it_p, rows_ms, segs_ms, rest_ms = pi.run_profiled(w["target"])
+        spmv_ms = rows_ms + segs_ms
         spmv_bytes = 12 * L + 16 * n  # per iteration: 4 B index + 8 B gathered z per edge; 8 B offset + 8 B sum per row
         rest_bytes = 48 * n           # update pass: read s, v, x, 1/deg; write x, z
         spmv_ach = spmv_bytes / (spmv_ms / it_p / 1000.0) / 1e9
@@ -437,6 +438,7 @@ def run_ours(args, world, rank, local):
                               "achieved": round(spmv_ach, 1), "peak": load_peaks()[0], "unit": "GB/s",
                               "frac": round(spmv_ach / load_peaks()[0], 4),
                               "bytes_per_iteration": spmv_bytes, "avg_iteration_ms": spmv_ms / it_p,
+                              "row_tiles_ms": rows_ms / it_p, "long_row_segments_ms": segs_ms / it_p,
                               "update_pass_ms": rest_ms / it_p,
                               "update_pass_frac": round(rest_bytes / (rest_ms / it_p / 1000.0) / 1e9
                                                         / load_peaks()[0], 4),
@@ -521,7 +523,7 @@ def run_ours(args, world, rank, local):
     # 64 personalization vectors x 10 seeds, every column to L1 residual 1e-9
     ppr = None
     if not args.no_ppr:
-        g4, _ = gen.generate(gen.web_config(8.0), 1_000_000, args.seed)
+        g4, _ = gen.baseline_graph(4, seed=args.seed)
         seeds = fr.config4_seeds(g4.n, 64, 10, seed=args.seed)
         pp = fr.BatchedPPR(g4, 64, 0.85, w["target"])
         pp.solve(seeds)  # warm-up (graph instantiation)

@@ -40,14 +40,14 @@ class PowerIteration:
         return x, int(iters.value), float(diff.value)
 
     def run_profiled(self, target_error, max_iterations=1_000_000):
-        """Same iterations launched from the host with CUDA events: (x, iterations,
-        spmv_ms, rest_ms) summed over the iterations (roofline report)."""
+        """Same iterations launched from the host with CUDA events: (x, iterations, rows_ms,
+        segs_ms, rest_ms) summed over the iterations (roofline report)."""
         x = torch.empty(self.graph.n, dtype=torch.float64, device=self.graph.out_offsets.device)
         iters = ctypes.c_int64(0)
-        ms = (ctypes.c_double * 2)()
+        ms = (ctypes.c_double * 3)()
         check(lib.fr_power_run_profiled(self.handle, float(target_error), int(max_iterations), ptr(x),
                                         ctypes.byref(iters), ms, stream_ptr()))
-        return x, int(iters.value), ms[0], ms[1]
+        return x, int(iters.value), ms[0], ms[1], ms[2]
 
     def close(self):
         if self.handle:

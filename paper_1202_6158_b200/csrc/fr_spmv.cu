@@ -429,9 +429,9 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
 }
 
 // The same iterations launched one by one from the host with CUDA events around
-// the SpMV (k_pi_rows + k_pi_segs) and the rest (mass, update, check): the
-// roofline report of bench.py, not the timed path.  h_ms[0] / h_ms[1] = summed
-// device time of the two classes.
+// each kernel class: the roofline report of bench.py, not the timed path.
+// h_ms[0] = short-row tiles (k_pi_rows), h_ms[1] = long-row segments (k_pi_segs),
+// h_ms[2] = the rest (dangling mass, update, check), summed over the iterations.
 extern "C" int fr_power_run_profiled(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
                                      int64_t *h_iterations, double *h_ms, void *stream) {
     if (!p || !(target_error > 0.0) || !d_x || !h_ms) {
@@ -443,31 +443,32 @@ extern "C" int fr_power_run_profiled(fr_power *p, double target_error, int64_t m
     a.in_graph = 0;
     a.target = target_error;
     a.max_iter = max_iterations > 0 ? max_iterations : 1000000;
-    cudaEvent_t ev[3];
-    for (int i = 0; i < 3; i++) FR_CUDA(cudaEventCreate(&ev[i]));
-    h_ms[0] = h_ms[1] = 0.0;
+    cudaEvent_t ev[4];
+    for (int i = 0; i < 4; i++) FR_CUDA(cudaEventCreate(&ev[i]));
+    h_ms[0] = h_ms[1] = h_ms[2] = 0.0;
     k_pi_init<<<p->grid, PI_NT, 0, st>>>(a);
     PiCtl hc = {};
     for (;;) {
         FR_CUDA(cudaEventRecord(ev[0], st));
         k_pi_rows<<<p->grid, PI_NT, 0, st>>>(a);
-        k_pi_segs<<<p->grid, PI_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[1], st));
+        k_pi_segs<<<p->grid, PI_NT, 0, st>>>(a);
+        FR_CUDA(cudaEventRecord(ev[2], st));
         k_pi_mass<<<1, PI_NT, 0, st>>>(a);
         k_pi_update<<<p->grid, PI_NT, 0, st>>>(a);
         k_pi_check<<<1, PI_NT, 0, st>>>(a);
-        FR_CUDA(cudaEventRecord(ev[2], st));
+        FR_CUDA(cudaEventRecord(ev[3], st));
         FR_CUDA(cudaGetLastError());
         FR_CUDA(cudaMemcpyAsync(&hc, p->ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
         FR_CUDA(cudaStreamSynchronize(st));
-        float t0 = 0.f, t1 = 0.f;
-        FR_CUDA(cudaEventElapsedTime(&t0, ev[0], ev[1]));
-        FR_CUDA(cudaEventElapsedTime(&t1, ev[1], ev[2]));
-        h_ms[0] += t0;
-        h_ms[1] += t1;
+        for (int k = 0; k < 3; k++) {
+            float t = 0.f;
+            FR_CUDA(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
+            h_ms[k] += t;
+        }
         if (hc.stop) break;
     }
-    for (int i = 0; i < 3; i++) cudaEventDestroy(ev[i]);
+    for (int i = 0; i < 4; i++) cudaEventDestroy(ev[i]);
     FR_CUDA(cudaMemcpyAsync(d_x, p->a.x, sizeof(double) * (size_t)p->n, cudaMemcpyDeviceToDevice, st));
     FR_CUDA(cudaStreamSynchronize(st));
     if (h_iterations) *h_iterations = (int64_t)hc.iters;

@@ -30,7 +30,7 @@ ap.add_argument("--local-frac", type=float, default=0.7)
 ap.add_argument("--window", type=int, default=1000)
 args = ap.parse_args()
 
-g, rep = gen.generate(gen.web_config(args.mean, local_frac=args.local_frac, window=args.window), args.n, 0)
+g, rep = gen.generate(gen.web_config(args.mean, local_frac=args.local_frac, window=args.window), args.n, 0, exact=True)
 params = fr.DiffusionParams(target_error=1e-9)
 state = fr.init(g, params, fluid_dtype=torch.float32 if args.fluid == "fp32" else torch.float64)
 solver = fr.Solver(g, state, fr.make_scheduler("sweep", policy=args.policy, sweep_decay=args.decay, kernel_path=args.path, hot_slots=args.hot_slots, warm_slots=args.warm_slots,
