@@ -438,7 +438,7 @@ def run_ours(args, world, rank, local):
                               "achieved": round(spmv_ach, 1), "peak": load_peaks()[0], "unit": "GB/s",
                               "frac": round(spmv_ach / load_peaks()[0], 4),
                               "bytes_per_iteration": spmv_bytes, "avg_iteration_ms": spmv_ms / it_p,
-                              "row_tiles_ms": rows_ms / it_p, "long_row_segments_ms": segs_ms / it_p,
+                              "short_rows_ms": rows_ms / it_p, "hub_rows_by_source_block_ms": segs_ms / it_p,
                               "update_pass_ms": rest_ms / it_p,
                               "update_pass_frac": round(rest_bytes / (rest_ms / it_p / 1000.0) / 1e9
                                                         / load_peaks()[0], 4),

@@ -235,7 +235,8 @@ int fr_power_run(fr_power *p, double target_error, int64_t max_iterations, doubl
                  int64_t *h_iterations, double *h_diff, void *stream);
 /* Same iterations launched from the host with CUDA events (roofline report, not
  * the timed path), summed over the iterations: h_ms[0] = short-row SpMV tiles,
- * h_ms[1] = long-row segments, h_ms[2] = the rest (dangling mass, update, check). */
+ * h_ms[1] = hub rows (in-degree > 1024) by source block, h_ms[2] = the rest
+ * (dangling mass, update, check). */
 int fr_power_run_profiled(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
                           int64_t *h_iterations, double *h_ms, void *stream);
 int fr_power_destroy(fr_power *p);

@@ -41,7 +41,8 @@ class PowerIteration:
 
     def run_profiled(self, target_error, max_iterations=1_000_000):
         """Same iterations launched from the host with CUDA events: (x, iterations, rows_ms,
-        segs_ms, rest_ms) summed over the iterations (roofline report)."""
+        hubs_ms, rest_ms) summed over the iterations (roofline report): short rows, hub rows
+        regrouped by source block, and the update pass."""
         x = torch.empty(self.graph.n, dtype=torch.float64, device=self.graph.out_offsets.device)
         iters = ctypes.c_int64(0)
         ms = (ctypes.c_double * 3)()

@@ -147,6 +147,9 @@ __device__ __forceinline__ u64 hmix(u64 z) {
 }
 
 static constexpr u32 HOT_FLAG = 0x80000000u;
+#ifndef FR_BLK_COLD
+#define FR_BLK_COLD 1
+#endif
 
 // ------------------------------------------------------------------ prologue
 // Exact sum |F| and max score.  guarded: only when the fused path asked for a check.
@@ -242,6 +245,20 @@ __device__ __forceinline__ void push_one(FT *__restrict__ F, FT *__restrict__ Fw
     } else {
         red_add(F + t, v);
     }
+}
+
+// push_one for a pusher far from its targets (hub rows): unslotted targets more
+// than 4096 ids from the source get the L2 evict-first hint (random lines)
+template <typename FT>
+__device__ __forceinline__ void push_far(FT *__restrict__ F, FT *__restrict__ Fw, FT *hot_acc, u32 nhot, u32 t,
+                                         FT v, bool slotted, u32 node, u64 pol) {
+#if FR_BLK_COLD
+    if (!(slotted && (t & HOT_FLAG)) && (t - node + 4096u) > 8192u) {
+        red_add_hint(F + t, v, pol);
+        return;
+    }
+#endif
+    push_one(F, Fw, hot_acc, nhot, t, v, slotted);
 }
 
 template <typename FT>
@@ -574,7 +591,7 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #define FR_OWN_UNROLL 3  // column loads in flight per lane and batch (k_sweep: FR_SW_UNROLL)
 #endif
 #ifndef FR_COLD_HINT
-#define FR_COLD_HINT 0
+#define FR_COLD_HINT 1
 #endif
 #ifndef FR_OWN_SKIPSCAN
 #define FR_OWN_SKIPSCAN 0
@@ -1014,6 +1031,7 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
     __shared__ FT hot_acc[HOT_SLOTS];
     const u32 cnt = a.ctl->qcount[2];
     if (blockIdx.x >= cnt) return;
+    const u64 pol = FR_BLK_COLD ? policy_evict_first() : 0ull;
     if (threadIdx.x == 0) {
         for (int s = 0; s < BLK_STAGES; s++) mbar_init(&bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1027,8 +1045,10 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
         const u64 lo = a.off[node], hi = a.off[node + 1];
         const u64 a0 = min(hi, (lo + 3) & ~3ull);
         const u64 a1 = max(a0, hi & ~3ull);
-        if (lo + threadIdx.x < a0) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + lo + threadIdx.x), v, a.nslots != 0);
-        if (a1 + threadIdx.x < hi) push_one(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + a1 + threadIdx.x), v, a.nslots != 0);
+        if (lo + threadIdx.x < a0)
+            push_far(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + lo + threadIdx.x), v, a.nslots != 0, node, pol);
+        if (a1 + threadIdx.x < hi)
+            push_far(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + a1 + threadIdx.x), v, a.nslots != 0, node, pol);
         const u64 body = a1 - a0;
         const u32 nch = (u32)((body + BLK_CHUNK - 1) / BLK_CHUNK);
         if (threadIdx.x == 0) {
@@ -1052,7 +1072,8 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
             const u32 len = (u32)min((u64)BLK_CHUNK, body - (u64)c * BLK_CHUNK);
             const u32 *sp = stage[s];
 #pragma unroll 4
-            for (u32 k = threadIdx.x; k < len; k += BLK_NT) push_one(a.F, a.Fw, hot_acc, a.nhot, sp[k], v, a.nslots != 0);
+            for (u32 k = threadIdx.x; k < len; k += BLK_NT)
+                push_far(a.F, a.Fw, hot_acc, a.nhot, sp[k], v, a.nslots != 0, node, pol);
             __syncthreads();  // slot s is free for the next bulk load
         }
         seq += nch;

@@ -6,8 +6,14 @@
 // reference's graph.to_matrix(), graph.py:158-165):
 //   s_i = sum_{j in in(i)} z_j,   z_j = x_j / outdeg_j (0 for dangling j)
 // Short rows: warp per tile of 32 rows over the tile's compacted edge space
-// (k_pi_rows).  Rows longer than LONG_ROW are split into warp-sized segments
-// whose partial sums are combined with atomics.
+// (k_pi_rows<false>).  Hub rows (in-degree > LONG_ROW: the Zipf in-degree hubs,
+// whose parents are spread over all ids) are regrouped by SOURCE BLOCK: hub row
+// h's sources are ascending, so its parents in block b (2^PI_SB ids, 2 MB of z)
+// are one contiguous slice of in_src, "row (b, h)".  The (b, h) rows are
+// processed block-major (k_pi_rows<true> and, for slices longer than LONG_ROW,
+// k_pi_segs), so the warps in flight gather from a few blocks' worth of z that
+// stays in L2 -- instead of one random 64 B DRAM burst per 8 B gathered -- and
+// add their sums into the hub's s (25k hubs on config 5: L2-resident).
 // The iteration loop is a CUDA-graph while-node (no host round trip).
 #include <math.h>
 
@@ -21,6 +27,10 @@ namespace fr {
 static constexpr int PI_NT = 256;
 static constexpr u64 LONG_ROW = 1024;
 static constexpr u64 SEG = 2048;
+#ifndef FR_PI_SB
+#define FR_PI_SB 18
+#endif
+static constexpr int PI_SB = FR_PI_SB;  // source block: 2^18 ids = 2 MB of z
 
 struct PiCtl {
     double c;       // teleport re-injection 1 - sum(y)
@@ -37,7 +47,13 @@ struct PiArgs {
     const double *inv;  // 1/outdeg or 0
     const double *v;
     double *x, *z, *s;
-    const u64 *seg_row, *seg_lo, *seg_hi;
+    // hub rows regrouped by source block: row (b, h) = b * nhub + h is the slice
+    // in_src[h_lo[r], h_lo[r] + h_cnt[r]) of hub row hub_node[h]
+    const u64 *h_lo;
+    const u32 *h_cnt, *hub_node;
+    long long h_rows;
+    u32 nhub;
+    const u64 *seg_row, *seg_lo, *seg_hi;  // (b, h) slices longer than LONG_ROW, seg_row = hub node
     long long nseg;
     double *part_s, *part_d;
     int nparts;
@@ -70,7 +86,11 @@ __global__ void __launch_bounds__(PI_NT) k_pi_init(PiArgs a) {
 // shared-memory accumulator when it walks past the row's end.  Per-lane work is
 // E/32 edges whatever the degree mix, and the 32-row tiles of a grid-stride
 // round are adjacent, so the gathered window of z stays in L2.
-static constexpr int PI_UNROLL = 4;
+#ifndef FR_PI_UNROLL
+#define FR_PI_UNROLL 4
+#endif
+static constexpr int PI_UNROLL = FR_PI_UNROLL;
+template <bool HUB>
 __global__ void __launch_bounds__(PI_NT) k_pi_rows(PiArgs a) {
     constexpr u32 FULL = 0xffffffffu;
     constexpr int NW = PI_NT / 32;
@@ -79,16 +99,22 @@ __global__ void __launch_bounds__(PI_NT) k_pi_rows(PiArgs a) {
     __shared__ double s_acc[NW][32];
     __shared__ double sm[NW];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const long long ntiles = (a.n + 31) / 32;
+    const long long nrows = HUB ? a.h_rows : a.n;
+    const long long ntiles = (nrows + 31) / 32;
     const long long nwarps = (long long)gridDim.x * NW;
     double acc_block = 0.0;
     for (long long t = blockIdx.x * (long long)NW + w; t < ntiles; t += nwarps) {
         const long long r = t * 32 + lane;
         u64 lo = 0, deg = 0;
-        if (r < a.n) {
-            lo = a.in_off[r];
-            deg = a.in_off[r + 1] - lo;
-            if (deg > LONG_ROW) deg = 0;
+        if (r < nrows) {
+            if (HUB) {
+                lo = a.h_lo[r];
+                deg = a.h_cnt[r];
+            } else {
+                lo = a.in_off[r];
+                deg = a.in_off[r + 1] - lo;
+            }
+            if (deg > LONG_ROW) deg = 0;  // hub rows (short kernel) / long slices (k_pi_segs)
         }
         u32 inc = (u32)deg;
 #pragma unroll
@@ -155,14 +181,15 @@ __global__ void __launch_bounds__(PI_NT) k_pi_rows(PiArgs a) {
             if (acc != 0.0) atomicAdd(&s_acc[w][k], acc);
         }
         __syncwarp();
-        if (r < a.n) {
+        if (r < nrows) {
             const double v = s_acc[w][lane];
-            a.s[r] = v;  // 0 for long rows: their segments accumulate next
+            if (!HUB) a.s[r] = v;  // 0 for hub rows: their (b, h) slices accumulate next
+            else if (v != 0.0) atomicAdd(a.s + a.hub_node[(u64)r % a.nhub], v);
             acc_block += v;
         }
     }
     acc_block = block_sum<PI_NT>(acc_block, sm);
-    if (threadIdx.x == 0) a.part_s[blockIdx.x] = acc_block;
+    if (threadIdx.x == 0) a.part_s[(HUB ? 2 * a.nparts : 0) + blockIdx.x] = acc_block;
 }
 
 // Warp per segment of a long row.
@@ -188,7 +215,7 @@ __global__ void __launch_bounds__(PI_NT) k_pi_segs(PiArgs a) {
 __global__ void __launch_bounds__(PI_NT) k_pi_mass(PiArgs a) {
     __shared__ double sm[PI_NT / 32];
     double t = 0.0;
-    for (int p = threadIdx.x; p < 2 * a.nparts; p += PI_NT) t += a.part_s[p];
+    for (int p = threadIdx.x; p < 3 * a.nparts; p += PI_NT) t += a.part_s[p];
     t = block_sum<PI_NT>(t, sm);
     if (threadIdx.x == 0) {
         const double ysum = a.d * t + (1.0 - a.d) * a.ctl->sum_v;
@@ -196,17 +223,46 @@ __global__ void __launch_bounds__(PI_NT) k_pi_mass(PiArgs a) {
     }
 }
 
+// x, z, s, v, inv are distinct arrays: the restrict-qualified copies let the
+// compiler keep PI_UPD loads of independent nodes in flight (the loop was one
+// node at a time behind the stores before)
+static constexpr int PI_UPD = 4;
 __global__ void __launch_bounds__(PI_NT) k_pi_update(PiArgs a) {
     __shared__ double sm[PI_NT / 32];
     const double c = a.ctl->c;
+    const double *__restrict__ v = a.v;
+    const double *__restrict__ s = a.s;
+    const double *__restrict__ inv = a.inv;
+    double *__restrict__ x = a.x;
+    double *__restrict__ z = a.z;
     double diff = 0.0;
-    for (long long i = blockIdx.x * (long long)PI_NT + threadIdx.x; i < a.n; i += (long long)gridDim.x * PI_NT) {
-        const double vi = a.v[i];
-        double y = a.d * a.s[i] + (1.0 - a.d) * vi;
+    const long long stride = (long long)gridDim.x * PI_NT;
+    long long i = blockIdx.x * (long long)PI_NT + threadIdx.x;
+    for (; i + (PI_UPD - 1) * stride < a.n; i += PI_UPD * stride) {
+        double vi[PI_UPD], si[PI_UPD], xi[PI_UPD], wi[PI_UPD];
+#pragma unroll
+        for (int u = 0; u < PI_UPD; u++) {
+            vi[u] = v[i + u * stride];
+            si[u] = s[i + u * stride];
+            xi[u] = x[i + u * stride];
+            wi[u] = inv[i + u * stride];
+        }
+#pragma unroll
+        for (int u = 0; u < PI_UPD; u++) {
+            double y = a.d * si[u] + (1.0 - a.d) * vi[u];
+            y += c * vi[u];
+            diff += fabs(y - xi[u]);
+            x[i + u * stride] = y;
+            z[i + u * stride] = y * wi[u];
+        }
+    }
+    for (; i < a.n; i += stride) {
+        const double vi = v[i];
+        double y = a.d * s[i] + (1.0 - a.d) * vi;
         y += c * vi;
-        diff += fabs(y - a.x[i]);
-        a.x[i] = y;
-        a.z[i] = y * a.inv[i];
+        diff += fabs(y - x[i]);
+        x[i] = y;
+        z[i] = y * inv[i];
     }
     diff = block_sum<PI_NT>(diff, sm);
     if (threadIdx.x == 0) a.part_d[blockIdx.x] = diff;
@@ -242,11 +298,31 @@ __global__ void k_long_rows(long long n, const u64 *__restrict__ off, u32 *list,
         if (off[i + 1] - off[i] > LONG_ROW) list[atomicAdd(count, 1u)] = (u32)i;
 }
 
-__global__ void k_row_bounds(const u32 *__restrict__ rows, u32 cnt, const u64 *__restrict__ off, u64 *out) {
-    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < cnt) {
-        out[2 * k] = off[rows[k]];
-        out[2 * k + 1] = off[rows[k] + 1];
+// Parents of hub row h per source block: h_cnt[(j >> PI_SB) * H + h] (warp per
+// hub row; the sources are ascending, so a warp's keys come in runs)
+__global__ void k_hub_count(const u32 *__restrict__ hub, u32 H, const u64 *__restrict__ in_off,
+                            const u32 *__restrict__ in_src, u32 *__restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const u32 nw = gridDim.x * (blockDim.x >> 5);
+    for (u32 h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); h < H; h += nw) {
+        const u64 lo = in_off[hub[h]], hi = in_off[hub[h] + 1];
+        for (u64 k0 = lo; k0 < hi; k0 += 32) {
+            const bool v = k0 + lane < hi;
+            const u64 key = v ? (u64)(in_src[k0 + lane] >> PI_SB) * H + h : ~0ull;
+            const u32 same = __match_any_sync(0xffffffffu, key);
+            if (v && lane == __ffs(same) - 1) atomicAdd(cnt + key, (u32)__popc(same));
+        }
+    }
+}
+// Start of slice (b, h) in in_src: hub row start + parents in blocks before b.
+__global__ void k_hub_lo(const u32 *__restrict__ hub, u32 H, long long nb, const u64 *__restrict__ in_off,
+                         const u32 *__restrict__ cnt, u64 *__restrict__ lo) {
+    for (u32 h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
+        u64 pos = in_off[hub[h]];
+        for (long long b = 0; b < nb; b++) {
+            lo[(u64)b * H + h] = pos;
+            pos += cnt[(u64)b * H + h];
+        }
     }
 }
 
@@ -259,6 +335,7 @@ struct fr_power {
     PiArgs a;
     double *buf;
     u64 *segbuf;
+    void *hubbuf;
     PiCtl *ctl;
     cudaGraph_t graph;
     cudaGraphExec_t exec;
@@ -296,9 +373,10 @@ static int power_build_graph(fr_power *p) {
     cp.conditional.size = 1;
     FR_CUDA(cudaGraphAddNode(&n_while, p->graph, &n_init, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    cudaGraphNode_t n1, n2, n3, n4, n5;
-    FR_TRY(add_node(body, &n1, nullptr, (void *)k_pi_rows, p->grid, args));
-    FR_TRY(add_node(body, &n2, &n1, (void *)k_pi_segs, p->grid, args));
+    cudaGraphNode_t n1, n1h, n2, n3, n4, n5;
+    FR_TRY(add_node(body, &n1, nullptr, (void *)k_pi_rows<false>, p->grid, args));
+    FR_TRY(add_node(body, &n1h, &n1, (void *)k_pi_rows<true>, p->grid, args));
+    FR_TRY(add_node(body, &n2, &n1h, (void *)k_pi_segs, p->grid, args));
     FR_TRY(add_node(body, &n3, &n2, (void *)k_pi_mass, 1, args));
     FR_TRY(add_node(body, &n4, &n3, (void *)k_pi_update, p->grid, args));
     FR_TRY(add_node(body, &n5, &n4, (void *)k_pi_check, 1, args));
@@ -312,6 +390,7 @@ extern "C" int fr_power_destroy(fr_power *p) {
     if (p->graph) cudaGraphDestroy(p->graph);
     cudaFree(p->buf);
     cudaFree(p->segbuf);
+    cudaFree(p->hubbuf);
     cudaFree(p->ctl);
     delete p;
     return FR_OK;
@@ -342,7 +421,7 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
         a.nparts = p->grid;
         cudaError_t e;
         // inv, v, x, z, s + partials
-        if ((e = cudaMalloc(&p->buf, sizeof(double) * (5 * (size_t)n + 3 * (size_t)p->grid))) != cudaSuccess ||
+        if ((e = cudaMalloc(&p->buf, sizeof(double) * (5 * (size_t)n + 4 * (size_t)p->grid))) != cudaSuccess ||
             (e = cudaMalloc(&p->ctl, sizeof(PiCtl))) != cudaSuccess) {
             rc = cuda_fail(e, "cudaMalloc(power)", __FILE__, __LINE__);
             break;
@@ -353,8 +432,8 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
         a.x = v + n;
         a.z = a.x + n;
         a.s = a.z + n;
-        a.part_s = a.s + n;           // 2 * grid (rows + segments)
-        a.part_d = a.part_s + 2 * p->grid;
+        a.part_s = a.s + n;           // 3 * grid (short rows, segments, hub slices)
+        a.part_d = a.part_s + 3 * p->grid;
         a.ctl = p->ctl;
         k_pi_inv<<<p->grid, PI_NT, 0, st>>>(n, reinterpret_cast<const u64 *>(d_out_offsets), inv);
         if (d_teleport) {
@@ -374,7 +453,7 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
             rc = cuda_fail(e, "ctl", __FILE__, __LINE__);
             break;
         }
-        // long-row segments
+        // hub rows: in-degree > LONG_ROW
         Scratch scratch(st);
         u32 *d_list, *d_cnt;
         if ((rc = scratch.alloc(&d_list, (size_t)std::min<long long>(n, m / (long long)LONG_ROW + 1))) != FR_OK) break;
@@ -384,24 +463,42 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
         u32 nlong = 0;
         cudaMemcpyAsync(&nlong, d_cnt, sizeof(u32), cudaMemcpyDeviceToHost, st);
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "long rows", __FILE__, __LINE__); break; }
-        std::vector<u32> rows(nlong);
-        std::vector<u64> lo(nlong), hi(nlong);
+        // hub rows regrouped by source block (k_pi_rows<true>, k_pi_segs)
         std::vector<u64> seg_row, seg_lo, seg_hi;
+        const long long nb = (n + (1ll << PI_SB) - 1) >> PI_SB;
+        a.nhub = nlong;
+        a.h_rows = nlong ? nb * (long long)nlong : 0;
         if (nlong) {
-            u64 *d_bounds;
-            if ((rc = scratch.alloc(&d_bounds, 2 * (size_t)nlong)) != FR_OK) break;
-            k_row_bounds<<<(nlong + 255) / 256, 256, 0, st>>>(d_list, nlong, a.in_off, d_bounds);
-            std::vector<u64> bounds(2 * (size_t)nlong);
-            cudaMemcpyAsync(rows.data(), d_list, sizeof(u32) * nlong, cudaMemcpyDeviceToHost, st);
-            cudaMemcpyAsync(bounds.data(), d_bounds, sizeof(u64) * 2 * nlong, cudaMemcpyDeviceToHost, st);
-            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "row bounds", __FILE__, __LINE__); break; }
-            for (u32 k = 0; k < nlong; k++) {
-                lo[k] = bounds[2 * k];
-                hi[k] = bounds[2 * k + 1];
-                for (u64 b = lo[k]; b < hi[k]; b += SEG) {
-                    seg_row.push_back(rows[k]);
+            const size_t R = (size_t)a.h_rows;
+            if ((e = cudaMalloc(&p->hubbuf, sizeof(u32) * ((size_t)nlong + R) + sizeof(u64) * R + 16)) !=
+                cudaSuccess) {
+                rc = cuda_fail(e, "cudaMalloc(hub slices)", __FILE__, __LINE__);
+                break;
+            }
+            u64 *h_lo = (u64 *)p->hubbuf;
+            u32 *h_cnt = (u32 *)(h_lo + R);
+            u32 *hub = h_cnt + R;
+            cudaMemcpyAsync(hub, d_list, sizeof(u32) * nlong, cudaMemcpyDeviceToDevice, st);
+            cudaMemsetAsync(h_cnt, 0, sizeof(u32) * R, st);
+            k_hub_count<<<p->grid, PI_NT, 0, st>>>(hub, nlong, a.in_off, a.in_src, h_cnt);
+            k_hub_lo<<<(nlong + 255) / 256, 256, 0, st>>>(hub, nlong, nb, a.in_off, h_cnt, h_lo);
+            a.h_lo = h_lo;
+            a.h_cnt = h_cnt;
+            a.hub_node = hub;
+            // slices longer than LONG_ROW become warp segments (host list, once)
+            std::vector<u32> cnt(R), hubs(nlong);
+            std::vector<u64> los(R);
+            cudaMemcpyAsync(cnt.data(), h_cnt, sizeof(u32) * R, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(los.data(), h_lo, sizeof(u64) * R, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(hubs.data(), hub, sizeof(u32) * nlong, cudaMemcpyDeviceToHost, st);
+            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "hub slices", __FILE__, __LINE__); break; }
+            for (size_t r = 0; r < R; r++) {
+                if (cnt[r] <= LONG_ROW) continue;
+                const u64 lo = los[r], hi = lo + cnt[r];
+                for (u64 b = lo; b < hi; b += SEG) {
+                    seg_row.push_back(hubs[r % nlong]);
                     seg_lo.push_back(b);
-                    seg_hi.push_back(std::min(hi[k], b + SEG));
+                    seg_hi.push_back(std::min(hi, b + SEG));
                 }
             }
         }
@@ -430,8 +527,9 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
 
 // The same iterations launched one by one from the host with CUDA events around
 // each kernel class: the roofline report of bench.py, not the timed path.
-// h_ms[0] = short-row tiles (k_pi_rows), h_ms[1] = long-row segments (k_pi_segs),
-// h_ms[2] = the rest (dangling mass, update, check), summed over the iterations.
+// h_ms[0] = short rows (k_pi_rows<false>), h_ms[1] = hub rows by source block
+// (k_pi_rows<true> + k_pi_segs), h_ms[2] = the rest (dangling mass, update,
+// check), summed over the iterations.
 extern "C" int fr_power_run_profiled(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
                                      int64_t *h_iterations, double *h_ms, void *stream) {
     if (!p || !(target_error > 0.0) || !d_x || !h_ms) {
@@ -450,8 +548,9 @@ extern "C" int fr_power_run_profiled(fr_power *p, double target_error, int64_t m
     PiCtl hc = {};
     for (;;) {
         FR_CUDA(cudaEventRecord(ev[0], st));
-        k_pi_rows<<<p->grid, PI_NT, 0, st>>>(a);
+        k_pi_rows<false><<<p->grid, PI_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[1], st));
+        k_pi_rows<true><<<p->grid, PI_NT, 0, st>>>(a);
         k_pi_segs<<<p->grid, PI_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[2], st));
         k_pi_mass<<<1, PI_NT, 0, st>>>(a);

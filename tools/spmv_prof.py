@@ -25,6 +25,6 @@ pi = fr.PowerIteration(g, fr.DiffusionParams(target_error=1e-9))
 pi.run_profiled(1e-9, 2)  # warm-up
 x, it, rows, segs, rest = pi.run_profiled(1e-9, args.iters or 1_000_000)
 L = g.edge_count
-print(f"n={g.n} L={L} iterations={it} per iteration: rows {rows / it:.3f} ms  segs {segs / it:.3f} ms  "
+print(f"n={g.n} L={L} iterations={it} per iteration: short rows {rows / it:.3f} ms  hub rows {segs / it:.3f} ms  "
       f"rest {rest / it:.3f} ms  spmv GB/s (12 B/edge + 16 B/row) "
       f"{(12 * L + 16 * g.n) / ((rows + segs) / it / 1e3) / 1e9:.0f}")
