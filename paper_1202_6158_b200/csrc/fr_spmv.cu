@@ -32,13 +32,27 @@ static constexpr u64 SEG = 2048;
 #endif
 static constexpr int PI_SB = FR_PI_SB;  // source block: 2^18 ids = 2 MB of z
 
+#ifndef FR_PI_SEGS
+#define FR_PI_SEGS 16
+#endif
+static constexpr int PI_SEGS = FR_PI_SEGS;  // in-order fronts of the row kernels
+static constexpr int PI_PAD = 16;           // u64 per counter: one 128 B line each
+static constexpr u32 PI_CHUNK = 4;          // tiles per claim
+
 struct PiCtl {
     double c;       // teleport re-injection 1 - sum(y)
     double diff;
     double sum_v;
     u64 iters;
     u32 stop;
+    u32 pad;
+    u64 seg_next[2][PI_SEGS * PI_PAD];  // row kernels (short, hub): next tile of each front
 };
+
+// zero the tile counters of both row kernels (one block)
+__device__ __forceinline__ void reset_fronts(PiCtl *c) {
+    for (int q = threadIdx.x; q < 2 * PI_SEGS; q += blockDim.x) c->seg_next[q / PI_SEGS][(q % PI_SEGS) * PI_PAD] = 0;
+}
 
 struct PiArgs {
     long long n;
@@ -70,6 +84,7 @@ __global__ void __launch_bounds__(PI_NT) k_pi_init(PiArgs a) {
         a.x[i] = xi;
         a.z[i] = xi * a.inv[i];
     }
+    if (blockIdx.x == 0) reset_fronts(a.ctl);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.ctl->iters = 0;
         a.ctl->stop = 0;
@@ -90,8 +105,115 @@ __global__ void __launch_bounds__(PI_NT) k_pi_init(PiArgs a) {
 #define FR_PI_UNROLL 4
 #endif
 static constexpr int PI_UNROLL = FR_PI_UNROLL;
+#ifndef FR_PI_MINB
+#define FR_PI_MINB 1
+#endif
+// One 32-row tile (warp): the rows' compacted edge space split into 32 equal
+// contiguous chunks, one per lane (see k_pi_rows).  gather(j) returns z_j.
+template <bool HUB, typename G>
+__device__ __forceinline__ void pi_tile(const PiArgs &a, long long t, long long nrows, u32 *s_pre, u64 *s_lo,
+                                        double *s_acc, double &acc_block, G gather) {
+    constexpr u32 FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const long long r = t * 32 + lane;
+    u64 lo = 0, deg = 0;
+    if (r < nrows) {
+        if (HUB) {
+            lo = a.h_lo[r];
+            deg = a.h_cnt[r];
+        } else {
+            lo = a.in_off[r];
+            deg = a.in_off[r + 1] - lo;
+        }
+        if (deg > LONG_ROW) deg = 0;  // hub rows (short kernel) / long slices (k_pi_segs)
+    }
+    u32 inc = (u32)deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const u32 E = __shfl_sync(FULL, inc, 31);
+    __syncwarp();
+    s_pre[lane + 1] = inc;
+    if (lane == 0) s_pre[0] = 0;
+    s_lo[lane] = lo;
+    s_acc[lane] = 0.0;
+    __syncwarp();
+    const u32 chunk = (E + 31) >> 5;
+    u32 q = lane * chunk;
+    const u32 qe = min(E, q + chunk);
+    if (q < qe) {
+        // the row holding edge q: the largest k with pre[k] <= q
+        int k = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1)
+            if (s_pre[k + step] <= q) k += step;
+        u32 rend = s_pre[k + 1];
+        u64 base = s_lo[k] - s_pre[k];  // in_src position of edge q' of row k: base + q'
+        double acc = 0.0;
+        // software pipeline: the column indices of the next batch are loaded
+        // while the current batch's gathers are in flight (the load walk has
+        // its own row cursor lk / lre / lbs, ahead of the accumulate cursor)
+        int lk = k;
+        u32 lre = rend;
+        u64 lbs = base;
+        u32 lq = q;  // next edge whose index is loaded
+        auto load_batch = [&](u32 (&src)[PI_UNROLL]) {
+#pragma unroll
+            for (int j = 0; j < PI_UNROLL; j++) {
+                src[j] = 0;
+                if (lq < qe) {
+                    while (lq >= lre) {
+                        lk++;
+                        lre = s_pre[lk + 1];
+                        lbs = s_lo[lk] - s_pre[lk];
+                    }
+                    src[j] = __ldg(a.in_src + lbs + lq);
+                    lq++;
+                }
+            }
+        };
+        u32 srcA[PI_UNROLL], srcB[PI_UNROLL];
+        load_batch(srcA);
+        while (q < qe) {
+            double zv[PI_UNROLL];
+#pragma unroll
+            for (int j = 0; j < PI_UNROLL; j++) zv[j] = q + j < qe ? gather(srcA[j]) : 0.0;
+            load_batch(srcB);
+#pragma unroll
+            for (int j = 0; j < PI_UNROLL; j++) {
+                if (q < qe) {
+                    while (q >= rend) {  // left row k: hand its partial sum over
+                        if (acc != 0.0) atomicAdd(&s_acc[k], acc);
+                        acc = 0.0;
+                        k++;
+                        rend = s_pre[k + 1];
+                    }
+                    acc += zv[j];
+                    q++;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < PI_UNROLL; j++) srcA[j] = srcB[j];
+        }
+        if (acc != 0.0) atomicAdd(&s_acc[k], acc);
+    }
+    __syncwarp();
+    if (r < nrows) {
+        const double v = s_acc[lane];
+        if (!HUB) a.s[r] = v;  // 0 for hub rows: their (b, h) slices accumulate next
+        else if (v != 0.0) atomicAdd(a.s + a.hub_node[(u64)r % a.nhub], v);
+        acc_block += v;
+    }
+}
+
+// Short rows (HUB = false) and hub slices (HUB = true), warp per 32-row tile:
+// tiles are claimed in order from PI_SEGS contiguous fronts (PI_CHUNK per
+// claim), so the rows in flight -- and the z lines they gather -- stay within a
+// few narrow windows (a grid-stride walk lets the warps drift apart).
 template <bool HUB>
-__global__ void __launch_bounds__(PI_NT) k_pi_rows(PiArgs a) {
+__global__ void __launch_bounds__(PI_NT, FR_PI_MINB) k_pi_rows(PiArgs a) {
     constexpr u32 FULL = 0xffffffffu;
     constexpr int NW = PI_NT / 32;
     __shared__ u32 s_pre[NW][33];
@@ -101,92 +223,33 @@ __global__ void __launch_bounds__(PI_NT) k_pi_rows(PiArgs a) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long nrows = HUB ? a.h_rows : a.n;
     const long long ntiles = (nrows + 31) / 32;
-    const long long nwarps = (long long)gridDim.x * NW;
+    const long long seg_len = (ntiles + PI_SEGS - 1) / PI_SEGS;
+    u64 *next = a.ctl->seg_next[HUB ? 1 : 0];
+    int seg = (int)(((long long)blockIdx.x * NW + w) % PI_SEGS), misses = 0;
+    long long t = 0, t_end = 0;
     double acc_block = 0.0;
-    for (long long t = blockIdx.x * (long long)NW + w; t < ntiles; t += nwarps) {
-        const long long r = t * 32 + lane;
-        u64 lo = 0, deg = 0;
-        if (r < nrows) {
-            if (HUB) {
-                lo = a.h_lo[r];
-                deg = a.h_cnt[r];
-            } else {
-                lo = a.in_off[r];
-                deg = a.in_off[r + 1] - lo;
-            }
-            if (deg > LONG_ROW) deg = 0;  // hub rows (short kernel) / long slices (k_pi_segs)
-        }
-        u32 inc = (u32)deg;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 y = __shfl_up_sync(FULL, inc, o);
-            if (lane >= o) inc += y;
-        }
-        const u32 E = __shfl_sync(FULL, inc, 31);
-        __syncwarp();
-        s_pre[w][lane + 1] = inc;
-        if (lane == 0) s_pre[w][0] = 0;
-        s_lo[w][lane] = lo;
-        s_acc[w][lane] = 0.0;
-        __syncwarp();
-        const u32 chunk = (E + 31) >> 5;
-        u32 q = lane * chunk;
-        const u32 qe = min(E, q + chunk);
-        if (q < qe) {
-            // the row holding edge q: the largest k with pre[k] <= q
-            int k = 0;
-#pragma unroll
-            for (int step = 16; step >= 1; step >>= 1)
-                if (s_pre[w][k + step] <= q) k += step;
-            u32 rend = s_pre[w][k + 1];
-            u64 base = s_lo[w][k] - s_pre[w][k];  // in_src position of edge q' of row k: base + q'
-            double acc = 0.0;
-            while (q < qe) {
-                u32 src[PI_UNROLL];
-                double zv[PI_UNROLL];
-                {
-                    int kk = k;
-                    u32 re = rend;
-                    u64 bs = base;
-#pragma unroll
-                    for (int j = 0; j < PI_UNROLL; j++) {
-                        src[j] = 0;
-                        if (q + j < qe) {
-                            while (q + j >= re) {
-                                kk++;
-                                re = s_pre[w][kk + 1];
-                                bs = s_lo[w][kk] - s_pre[w][kk];
-                            }
-                            src[j] = __ldg(a.in_src + bs + q + j);
-                        }
-                    }
+    const double *__restrict__ z = a.z;
+    for (;;) {
+        if (t >= t_end) {
+            bool got = false;
+            while (misses < PI_SEGS) {
+                u64 k = 0;
+                if (lane == 0) k = atomicAdd(next + seg * PI_PAD, (u64)PI_CHUNK);
+                k = __shfl_sync(FULL, k, 0);
+                const long long s0 = seg * seg_len, s1 = min(ntiles, s0 + seg_len);
+                if (s0 + (long long)k < s1) {
+                    t = s0 + (long long)k;
+                    t_end = min(s1, t + (long long)PI_CHUNK);
+                    got = true;
+                    break;
                 }
-#pragma unroll
-                for (int j = 0; j < PI_UNROLL; j++) zv[j] = q + j < qe ? a.z[src[j]] : 0.0;
-#pragma unroll
-                for (int j = 0; j < PI_UNROLL; j++) {
-                    if (q < qe) {
-                        while (q >= rend) {  // left row k: hand its partial sum over
-                            if (acc != 0.0) atomicAdd(&s_acc[w][k], acc);
-                            acc = 0.0;
-                            k++;
-                            rend = s_pre[w][k + 1];
-                            base = s_lo[w][k] - s_pre[w][k];
-                        }
-                        acc += zv[j];
-                        q++;
-                    }
-                }
+                seg = (seg + 1) % PI_SEGS;
+                misses++;
             }
-            if (acc != 0.0) atomicAdd(&s_acc[w][k], acc);
+            if (!got) break;
         }
-        __syncwarp();
-        if (r < nrows) {
-            const double v = s_acc[w][lane];
-            if (!HUB) a.s[r] = v;  // 0 for hub rows: their (b, h) slices accumulate next
-            else if (v != 0.0) atomicAdd(a.s + a.hub_node[(u64)r % a.nhub], v);
-            acc_block += v;
-        }
+        pi_tile<HUB>(a, t, nrows, s_pre[w], s_lo[w], s_acc[w], acc_block, [&](u32 j) { return z[j]; });
+        t++;
     }
     acc_block = block_sum<PI_NT>(acc_block, sm);
     if (threadIdx.x == 0) a.part_s[(HUB ? 2 * a.nparts : 0) + blockIdx.x] = acc_block;
@@ -273,6 +336,7 @@ __global__ void __launch_bounds__(PI_NT) k_pi_check(PiArgs a) {
     double t = 0.0;
     for (int p = threadIdx.x; p < a.nparts; p += PI_NT) t += a.part_d[p];
     t = block_sum<PI_NT>(t, sm);
+    reset_fronts(a.ctl);
     if (threadIdx.x == 0) {
         PiCtl *c = a.ctl;
         c->diff = t;
