@@ -552,6 +552,12 @@ def run_ours(args, world, rank, local):
                                                     "(take, history r/w) + 4 B per edge visit + 8 B per pushed "
                                                     "column value",
                     "timing": "whole solve, CUDA events (k_ppr_sweep dominates)"}
+        try:
+            pt = json.load(open(os.path.join(ROOT, "profiles", "r02_ppr_traffic.json")))
+            ppr_roof["traffic"] = pt["dram_bytes_per_solve"]
+            ppr_roof["traffic_note"] = "ncu DRAM bytes of one whole solve (graph profiling), profiles/r02_ppr_traffic.json"
+        except Exception:
+            ppr_roof["traffic"] = None
         ppr = {"roofline": ppr_roof,"workload": "BASELINE configs[3]: N=1M web graph (mean out-degree 8, %d edges), 64 vectors x 10 "
                            "seeds, d=0.85, each column to L1 residual 1e-9, n x 64 fp64 row-major state" % g4.edge_count,
                "time_s": t4, "sweeps": st4.sweeps, "row_visits": st4.diffusions, "edge_visits": st4.elementary_steps,

@@ -16,8 +16,14 @@
 namespace fr {
 
 static constexpr int PP_NT = 256;
-static constexpr int PP_SEGS = 16;
-static constexpr int PP_CHUNK = 64;  // consecutive nodes per reservation (one warp per node)
+#ifndef FR_PP_SEGS
+#define FR_PP_SEGS 16
+#endif
+#ifndef FR_PP_CHUNK
+#define FR_PP_CHUNK 64
+#endif
+static constexpr int PP_SEGS = FR_PP_SEGS;
+static constexpr int PP_CHUNK = FR_PP_CHUNK;  // consecutive nodes per reservation (one warp per node)
 
 struct PprCtl {
     double theta;
@@ -27,7 +33,7 @@ struct PprCtl {
     u64 need_check;        // columns whose incremental residual crossed the target
     u64 diffusions, steps, sweeps;
     u64 pushes;            // column values scattered (one red.add each)
-    u64 seg_next[PP_SEGS];
+    u64 seg_next[PP_SEGS * 16];  // one 128 B line per front counter
     u32 stop;
     u32 pad;
 };
@@ -77,7 +83,7 @@ __global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
     auto grab = [&]() -> bool {
         while (misses < PP_SEGS) {
             unsigned long long k = 0;
-            if (lane == 0) k = atomicAdd(&c->seg_next[seg], (unsigned long long)PP_CHUNK);
+            if (lane == 0) k = atomicAdd(&c->seg_next[seg * 16], (unsigned long long)PP_CHUNK);
             k = __shfl_sync(FULL, k, 0);
             const long long s0 = (long long)seg * seg_len;
             const long long s1 = s0 + seg_len < a.n ? s0 + seg_len : a.n;
@@ -239,7 +245,7 @@ __global__ void k_ppr_finalize(PprArgs a) {
         c->diffusions += sel;
         c->steps += st;
         c->sweeps += 1;
-        for (int q = 0; q < PP_SEGS; q++) c->seg_next[q] = 0;
+        for (int q = 0; q < PP_SEGS; q++) c->seg_next[q * 16] = 0;
     }
     __syncthreads();
     if (col < a.B && ((c->active >> col) & 1ull)) {

@@ -1,0 +1,25 @@
+"""Batched-PPR profiling driver (BASELINE configs[3]): the exact config-4 graph, 64
+personalization vectors x 10 seeds, one warm-up and one profiled solve.  Under ncu use
+--graph-profiling graph (the solve is one CUDA graph with a while node).  Not a benchmark."""
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_1202_6158_b200 as fr  # noqa: E402
+from paper_1202_6158_b200 import gen  # noqa: E402
+
+g, _ = gen.baseline_graph(4)
+seeds = fr.config4_seeds(g.n, 64, 10, seed=0)
+p = fr.BatchedPPR(g, 64, 0.85, 1e-9)
+p.solve(seeds)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+rank, st, res = p.solve(seeds)
+e1.record()
+torch.cuda.synchronize()
+print(f"n={g.n} L={g.edge_count} time {e0.elapsed_time(e1):.2f} ms sweeps={st.sweeps} row_visits={st.diffusions} "
+      f"edge_visits={st.elementary_steps} pushes={st.hub_edges} max_residual={max(res):.2e}")

@@ -47,7 +47,7 @@ for k in ("k_sweep", "k_sweep_own", "k_push_block", "k_fold"):
         res[k + "_dram_gbs_under_ncu"] = round(a[2] / a[1] / 1e9) if a[1] else None
         res[k + "_launches"] = a[0]
 res["source"] = desc
-res["round"] = 1
+res["round"] = 2
 res["kernel_path"] = sys.argv[4] if len(sys.argv) > 4 else "owned"
 json.dump(res, open(out, "w"), indent=1)
 print("wrote", out)
