@@ -671,7 +671,7 @@ def main():
     ap.add_argument("--path", default="owned", choices=("fused", "binned", "owned"))
     ap.add_argument("--hot-slots", type=int, default=0, help="0 default (2048), -1 off")
     ap.add_argument("--warm-slots", type=int, default=0, help="0 default (2^21), -1 off")
-    ap.add_argument("--beta", type=float, default=0.65, help="degree exponent of the sweep score")
+    ap.add_argument("--beta", type=float, default=0.85, help="degree exponent of the sweep score")
     ap.add_argument("--fluid", default="fp64", choices=("fp64", "fp32"))
     ap.add_argument("--thread-max", type=int, default=0)
     ap.add_argument("--block-min", type=int, default=0)

@@ -10,7 +10,7 @@ oracle (oracle.gen_graph_exact, bit-exact with the reference loader's cleaning):
     the generator report) -- bit-exact or fail;
   * ranks: the device solve with the EXACT bench schedule (owned path, default chunks
     and slots, adaptive theta (0.6, 0.2) at d = 0.85 and (0.7, 0.15) at d = 0.99,
-    degree exponent 0.65, target 1e-9) against the oracle's sequential ALGO-REF +
+    degree exponent 0.85, target 1e-9) against the oracle's sequential ALGO-REF +
     ThresholdSweepScheduler run (oracle.run_seq, bit-exact with fluidrank.engine.run)
     at a tighter target: L1 <= 1e-9 in fp64, <= 1e-6 for the fp32-fluid variant;
   * config 5 also through the host-buffer entry point fr_pagerank_host (8-piece copy,
@@ -43,6 +43,7 @@ SCHED = {0.85: (0.6, 0.2), 0.99: (0.7, 0.15)}  # bench.py --decay/--edge-frac, -
 ORACLE_TRUTH = {0.85: 1e-12, 0.99: 1e-12}  # oracle targets of the "tight" solution
 GPU_TIGHT = {0.85: 1e-10, 0.99: 1e-11}     # the device solve re-run below the config's 1e-9
 PPR_COLUMNS = 8
+BETA = 0.85  # bench.py --beta
 
 
 def sha(a):
@@ -130,7 +131,7 @@ def gpu_config(cfg_index, results, futures):
         for d in dampings:
             decay, ef = SCHED[d]
             sched = fr.make_scheduler("sweep", policy="adaptive", sweep_decay=decay, edge_frac=ef,
-                                      degree_exponent=0.65)
+                                      degree_exponent=BETA)
             params = fr.DiffusionParams(damping=d, target_error=1e-9)
             legs = [("fp64", 1e-9), ("tight", GPU_TIGHT[d])] + ([("fp32", 1e-9)] if cfg_index == 3 else [])
             for fl, te in legs:
@@ -193,7 +194,7 @@ def main():
     torch.cuda.set_device(0)
     report = {"seed": SEED, "oracle": "oracle/fr_oracle.c run_seq (ALGO-REF + ThresholdSweepScheduler, bit-exact "
                                        "with fluidrank.engine.run) on oracle.gen_graph_exact",
-              "schedule": {"0.85": SCHED[0.85], "0.99": SCHED[0.99], "degree_exponent": 0.65,
+              "schedule": {"0.85": SCHED[0.85], "0.99": SCHED[0.99], "degree_exponent": BETA,
                            "kernel_path": "owned", "policy": "adaptive", "target_error": 1e-9},
               "bounds": {"fp64": 1e-9, "fp32_fluid": 1e-6}, "configs": {}}
     gpu_ranks = {}

@@ -26,7 +26,7 @@ ap.add_argument("--fluid", default="fp64")
 ap.add_argument("--path", default="fused")
 args = ap.parse_args()
 
-g, _ = gen.generate(gen.web_config(args.mean), args.n, 0)
+g, _ = gen.generate(gen.web_config(args.mean), args.n, 0, exact=True)
 fl = [float(x) for x in args.damping.split(",")]
 dl = [float(x) for x in args.decay.split(",")]
 bl = [float(x) for x in args.beta.split(",")]
