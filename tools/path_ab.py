@@ -19,7 +19,7 @@ ap.add_argument("--n", type=int, default=100_000_000)
 ap.add_argument("--mean", type=float, default=16.0)
 ap.add_argument("--damping", type=float, default=0.85)
 ap.add_argument("--decay", type=float, default=0.6)
-ap.add_argument("--beta", type=float, default=0.65)
+ap.add_argument("--beta", type=float, default=0.85)
 ap.add_argument("--edge-frac", type=float, default=0.2)
 ap.add_argument("--policy", default="adaptive")
 ap.add_argument("--fluid", default="fp64")

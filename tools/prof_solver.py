@@ -23,7 +23,7 @@ ap.add_argument("--fluid", default="fp64")
 ap.add_argument("--path", default="owned")
 ap.add_argument("--hot-slots", type=int, default=0)
 ap.add_argument("--block-min", type=int, default=0)
-ap.add_argument("--beta", type=float, default=0.65)
+ap.add_argument("--beta", type=float, default=0.85)
 ap.add_argument("--warm-slots", type=int, default=0)
 ap.add_argument("--graph", action="store_true", help="run the CUDA-graph path instead")
 ap.add_argument("--local-frac", type=float, default=0.7)
