@@ -1,10 +1,11 @@
 """BASELINE configs at full size.
 
-config 2 (N=1M) is small enough for the CPU oracle: bit-exact generator/CSR and
-rank parity.  config 3 (N=20M) is checked through size-independent
+config 2 (N=1M) is small enough for the CPU oracle here: bit-exact generator/CSR
+and rank parity.  config 3 (N=20M) is checked through size-independent
 properties: the fp64 D-iteration agrees with the independent power-iteration
-solver, the fp32-fluid variant stays within its stated tolerance of fp64, and
-the stopping rule and conservation hold.
+solver within 1e-9, the fp32-fluid variant stays within its stated tolerance
+of fp64, and the stopping rule and conservation hold.  The oracle comparison
+of configs 3-5 at full size is tests/fullsize_parity.py (test_gpu_fullsize.py).
 """
 
 import numpy as np
@@ -15,14 +16,16 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
 def test_config2_full_size_parity(cuda, oracle):
+    """The exact-size config-2 graph (base draw + fill rounds) bit-exact with the oracle's,
+    and the rank within 1e-9 of the sequential reference run."""
     from paper_1202_6158_b200 import gen
     n, seed = 1_000_000, 2
-    g, rep = gen.generate(gen.web_config(8.0), n, seed)
-    src, dst = oracle.gen_edges(oracle.web_config(8.0), n, seed)
-    off, tgt, stats = oracle.csr_build(n, src, dst, clean=True)
+    g, rep = gen.baseline_graph(2, seed=seed)
+    off, tgt, orep = oracle.gen_graph_exact(oracle.web_config(8.0), n, seed)
     assert np.array_equal(g.out_offsets.cpu().numpy(), off)
     assert np.array_equal(g.out_targets.cpu().numpy().astype(np.uint32), tgt)
-    assert (rep.realized_links, rep.duplicates, rep.self_loops) == stats
+    assert (rep.realized_links, rep.duplicates, rep.self_loops, rep.rounds, rep.unfilled) == (
+        orep["realized_links"], orep["duplicates"], orep["self_loops"], orep["rounds"], orep["unfilled"])
     params = cuda.DiffusionParams(target_error=1e-10)
     sched = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9)
     rank, trace = cuda.run(g, params, sched)
@@ -33,18 +36,24 @@ def test_config2_full_size_parity(cuda, oracle):
 
 def test_config3_fp32_tolerance_and_power_iteration(cuda):
     from paper_1202_6158_b200 import gen
-    g, rep = gen.generate(gen.web_config(10.0), 20_000_000, 3)
+    g, rep = gen.baseline_graph(3, seed=3)
     params = cuda.DiffusionParams(target_error=1e-9)
     sched = cuda.make_scheduler("sweep", policy="geometric", sweep_decay=0.9)
     state = cuda.init(g, params)
     r64, _ = cuda.run(g, params, sched, state=state)
     assert state.residual <= 1e-9 * 0.15
     assert abs(float(r64.sum()) - 1.0) < 1e-12
+    # stated tolerance of the fp32-fluid / fp64-history variant: 1e-6
+    # with the benchmarked schedule; the rounding grows with the pushes per node, so a
+    # slow plain-score schedule (geometric 0.9, ~3x the sweeps) gets 2e-6
     r32, _ = cuda.run(g, params, sched, fluid_dtype=torch.float32)
-    # stated tolerance of the fp32-fluid / fp64-history variant
-    assert float(np.abs(r32 - r64).sum()) <= 1e-6
+    assert float(np.abs(r32 - r64).sum()) <= 2e-6
+    bench = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.6, edge_frac=0.2, degree_exponent=0.85)
+    b64, _ = cuda.run(g, params, bench)
+    b32, _ = cuda.run(g, params, bench, fluid_dtype=torch.float32)
+    assert float(np.abs(b32 - b64).sum()) <= 1e-6
     x, trace = cuda.power_iterate(g, cuda.DiffusionParams(target_error=1e-10))
-    assert float(np.abs(x - r64).sum()) <= 5e-9
+    assert float(np.abs(x - r64).sum()) <= 1e-9
 
 
 @pytest.mark.parametrize("slots", ["default", "off"])
@@ -55,7 +64,7 @@ def test_config3_host_buffer_pieces(cuda, slots):
     caller's host arrays are untouched."""
     import ctypes
     from paper_1202_6158_b200 import _lib, gen
-    g, _ = gen.generate(gen.web_config(10.0), 20_000_000, 3)
+    g, _ = gen.baseline_graph(3, seed=3)
     params = cuda.DiffusionParams(target_error=1e-9)
     kw = dict(hot_slots=-1, warm_slots=-1) if slots == "off" else {}
     sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.7, degree_exponent=0.65, edge_frac=0.15,
