@@ -234,9 +234,10 @@ int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offsets, const in
 int fr_power_run(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
                  int64_t *h_iterations, double *h_diff, void *stream);
 /* Same iterations launched from the host with CUDA events (roofline report, not
- * the timed path), summed over the iterations: h_ms[0] = short-row SpMV tiles,
- * h_ms[1] = hub rows (in-degree > 1024) by source block, h_ms[2] = the rest
- * (dangling mass, update, check). */
+ * the timed path), summed over the iterations (h_ms: 4 doubles): h_ms[0] =
+ * short-row SpMV tiles with their rows' update, h_ms[1] = hub rows (in-degree >
+ * 1024) by source block, h_ms[2] = long hub slices, h_ms[3] = the rest (hub
+ * rows' update, stopping rule). */
 int fr_power_run_profiled(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
                           int64_t *h_iterations, double *h_ms, void *stream);
 int fr_power_destroy(fr_power *p);

@@ -41,14 +41,16 @@ class PowerIteration:
 
     def run_profiled(self, target_error, max_iterations=1_000_000):
         """Same iterations launched from the host with CUDA events: (x, iterations, rows_ms,
-        hubs_ms, rest_ms) summed over the iterations (roofline report): short rows, hub rows
-        regrouped by source block, and the update pass."""
+        hubs_ms, rest_ms) summed over the iterations (roofline report): short rows with
+        their update, hub rows regrouped by source block (slices and long segments), and
+        the hub rows' update with the stopping rule."""
         x = torch.empty(self.graph.n, dtype=torch.float64, device=self.graph.out_offsets.device)
         iters = ctypes.c_int64(0)
-        ms = (ctypes.c_double * 3)()
+        ms = (ctypes.c_double * 4)()
         check(lib.fr_power_run_profiled(self.handle, float(target_error), int(max_iterations), ptr(x),
                                         ctypes.byref(iters), ms, stream_ptr()))
-        return x, int(iters.value), ms[0], ms[1], ms[2]
+        self.last_profile_ms = {"short_rows": ms[0], "hub_slices": ms[1], "hub_segments": ms[2], "rest": ms[3]}
+        return x, int(iters.value), ms[0], ms[1] + ms[2], ms[3]
 
     def close(self):
         if self.handle:

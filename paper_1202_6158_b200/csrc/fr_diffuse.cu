@@ -596,6 +596,15 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #ifndef FR_OWN_SKIPSCAN
 #define FR_OWN_SKIPSCAN 0
 #endif
+#ifndef FR_OWN_BULKPF
+#define FR_OWN_BULKPF 0  // 1: one bulk L2 prefetch of the chunk's fluid and offsets instead of per-tile prefetches
+#endif
+#ifndef FR_OWN_RAWCLAIM
+#define FR_OWN_RAWCLAIM 0  // 1: tile claims by a plain atom.shared.add (no compiler warp aggregation)
+#endif
+#ifndef FR_OWN_FASTMAX
+#define FR_OWN_FASTMAX 0  // 1: running max score by compare-select (no NaN handling)
+#endif
 static constexpr int OWN_NT = FR_OWN_NT;
 static constexpr int OWN_UNROLL = FR_OWN_UNROLL;
 static_assert(OWN_UNROLL * 6 <= 32, "packed row indices");
@@ -658,6 +667,15 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
         const u32 len = (u32)((u64)a.n - (u64)base < CH ? (u64)a.n - (u64)base : CH);
         const u32 ntl = (len + 31) >> 5;
         auto tmap = [&](u32 lt) -> u32 { return rev ? ntl - 1 - lt : lt; };
+#if FR_OWN_BULKPF
+        if (threadIdx.x == 0) {
+            // the chunk's fluid and row offsets into L2 by two bulk prefetches (16 B granules)
+            const u32 fb = (len * (u32)sizeof(FT) + 15u) & ~15u;
+            const u32 ob = ((len + 1) * (u32)sizeof(OT) + 15u) & ~15u;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(F + base), "r"(fb) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(offp + base), "r"(ob) : "memory");
+        }
+#endif
         FT f_cur = (FT)0;
         OT lo_cur = 0, end_cur = 0;
         auto load_tile = [&](u32 lt, FT &fo, OT &loo, OT &endo) {
@@ -674,12 +692,17 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
         if (lt < ntl) load_tile(lt, f_cur, lo_cur, end_cur);
         while (lt < ntl) {
             u32 lnx = 0;
+#if FR_OWN_RAWCLAIM
+            if (lane == 0)
+                asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(lnx) : "r"((u32)__cvta_generic_to_shared(ctr)) : "memory");
+#else
             if (lane == 0) lnx = atomicAdd(ctr, 1u);
+#endif
             lnx = __shfl_sync(FULL, lnx, 0);
             FT f_nx = (FT)0;
             OT lo_nx = 0, end_nx = 0;
             if (lnx < ntl) load_tile(lnx, f_nx, lo_nx, end_nx);
-            {
+            if (!FR_OWN_BULKPF) {
                 const u32 pf = lnx + FR_OWN_PF * OWN_NW;
                 if (pf < ntl && lane < FR_OWN_PF_LANES) {
                     const IT j = base + (IT)(tmap(pf) << 5) + (lane & 1) * 16;
@@ -702,7 +725,11 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
             const double af = fabs((double)f);
             double score = (a.weight && valid) ? af * a.weight[i] : af;
             if (a.beta != 0.0f) score = af * deg_weight(a.beta, deg);
+#if FR_OWN_FASTMAX
+            mx = score > mx ? score : mx;
+#else
             mx = fmax(mx, score);
+#endif
             bool sel;
             if (a.select == FR_SELECT_PER) sel = true;
             else if (a.select == FR_SELECT_RAND)

@@ -40,7 +40,7 @@ static constexpr int PI_PAD = 16;           // u64 per counter: one 128 B line e
 static constexpr u32 PI_CHUNK = 4;          // tiles per claim
 
 struct PiCtl {
-    double c;       // teleport re-injection 1 - sum(y)
+    double c;       // teleport re-injection 1 - sum(y) of the coming iteration
     double diff;
     double sum_v;
     u64 iters;
@@ -59,18 +59,25 @@ struct PiArgs {
     const u64 *in_off;
     const u32 *in_src;
     const double *inv;  // 1/outdeg or 0
-    const double *v;
-    double *x, *z, *s;
+    const double *v;    // teleport (null: uniform v_const)
+    double v_const;
+    double *x;
+    double *zb[2];      // z = x/outdeg, double-buffered: iteration k gathers zb[k & 1], writes zb[(k + 1) & 1]
+    double *s_hub;      // [nhub] in-sums of the hub rows, added by the slice kernels
     // hub rows regrouped by source block: row (b, h) = b * nhub + h is the slice
-    // in_src[h_lo[r], h_lo[r] + h_cnt[r]) of hub row hub_node[h]
+    // hub_src[h_lo[r], h_lo[r] + h_cnt[r]) of hub row hub_node[h] -- a private copy of
+    // the hub rows' in-edges stored block-major, so the slices of consecutive (b, h)
+    // rows are contiguous (slices longer than LONG_ROW sit after them as segments)
+    const u32 *hub_src;
     const u64 *h_lo;
     const u32 *h_cnt, *hub_node;
     long long h_rows;
     u32 nhub;
-    const u64 *seg_row, *seg_lo, *seg_hi;  // (b, h) slices longer than LONG_ROW, seg_row = hub node
+    const u64 *seg_row, *seg_lo, *seg_hi;  // (b, h) slices longer than LONG_ROW, seg_row = hub index h
     long long nseg;
-    double *part_s, *part_d;
-    int nparts;
+    double *part_d, *part_nd;  // per-block |y - x|_1 and sum of y over non-dangling nodes
+    int nparts;                // row-kernel blocks; the hub update's blocks follow
+    int hub_grid;
     PiCtl *ctl;
     double d, target;
     long long max_iter;
@@ -78,45 +85,85 @@ struct PiArgs {
     cudaGraphConditionalHandle cond;
 };
 
+__device__ __forceinline__ const double *z_rd(const PiArgs &a, u64 it) { return a.zb[it & 1]; }
+__device__ __forceinline__ double *z_wr(const PiArgs &a, u64 it) { return a.zb[(it + 1) & 1]; }
+
+// baseline.py:41-43 for row i, with the re-injection c = 1 - sum(y) known before the
+// product: sum(P x) = sum of x over the non-dangling nodes (every column of P sums
+// to 1), so c follows from the previous update (k_pi_check) and the update is
+// fused into the row kernels (no separate pass over s, x, v, 1/deg)
+// (xi, w, vi: the row's x, 1/outdeg and teleport, loaded by the caller ahead of time)
+__device__ __forceinline__ void pi_update_row(const PiArgs &a, long long i, double s, double c, double *zw,
+                                              double xi, double w, double vi, double &diff, double &nd) {
+    double y = a.d * s + (1.0 - a.d) * vi;
+    y += c * vi;
+    diff += fabs(y - xi);
+    a.x[i] = y;
+    zw[i] = y * w;
+    if (w != 0.0) nd += y;
+}
+
 __global__ void __launch_bounds__(PI_NT) k_pi_init(PiArgs a) {
+    __shared__ double sm[PI_NT / 32];
+    double nd = 0.0;
     for (long long i = blockIdx.x * (long long)PI_NT + threadIdx.x; i < a.n; i += (long long)gridDim.x * PI_NT) {
-        const double xi = a.v[i];
+        const double xi = a.v ? a.v[i] : a.v_const;
+        const double w = a.inv[i];
         a.x[i] = xi;
-        a.z[i] = xi * a.inv[i];
+        a.zb[0][i] = xi * w;
+        if (w != 0.0) nd += xi;
     }
-    if (blockIdx.x == 0) reset_fronts(a.ctl);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (long long h = blockIdx.x * (long long)PI_NT + threadIdx.x; h < a.nhub; h += (long long)gridDim.x * PI_NT)
+        a.s_hub[h] = 0.0;
+    nd = block_sum<PI_NT>(nd, sm);
+    if (threadIdx.x == 0) {
+        a.part_nd[blockIdx.x] = nd;
+        a.part_d[blockIdx.x] = 0.0;
+    }
+}
+
+// c of the first iteration from the partials of k_pi_init (one block)
+__global__ void __launch_bounds__(PI_NT) k_pi_start(PiArgs a) {
+    __shared__ double sm[PI_NT / 32];
+    double t = 0.0;
+    for (int p = threadIdx.x; p < a.nparts; p += PI_NT) t += a.part_nd[p];
+    t = block_sum<PI_NT>(t, sm);
+    reset_fronts(a.ctl);
+    if (threadIdx.x == 0) {
+        a.ctl->c = 1.0 - (a.d * t + (1.0 - a.d) * a.ctl->sum_v);
         a.ctl->iters = 0;
         a.ctl->stop = 0;
         if (a.in_graph) cudaGraphSetConditional(a.cond, 1u);
     }
 }
 
-// Warp per tile of 32 consecutive rows; rows longer than LONG_ROW are left at 0
-// here (their warp segments add into them in k_pi_segs).  The tile's short rows
-// are contiguous ranges of in_src, so their concatenation (the tile's compacted
-// edge space, E edges) is split into 32 equal contiguous chunks, one per lane:
-// every lane streams its column indices in order with PI_UNROLL independent
-// loads and gathers in flight, and adds its partial sum of a row to the row's
-// shared-memory accumulator when it walks past the row's end.  Per-lane work is
-// E/32 edges whatever the degree mix, and the 32-row tiles of a grid-stride
-// round are adjacent, so the gathered window of z stays in L2.
+// Warp per tile of 32 consecutive rows; rows longer than LONG_ROW are skipped
+// here (their slices add into s_hub, k_pi_hub_update finishes them).  The tile's
+// short rows are contiguous ranges of in_src, so their concatenation (the tile's
+// compacted edge space, E edges) is split into 32 equal contiguous chunks, one
+// per lane: every lane streams its column indices in order with PI_UNROLL
+// independent loads and gathers in flight, and adds its partial sum of a row to
+// the row's shared-memory accumulator when it walks past the row's end.  Per-lane
+// work is E/32 edges whatever the degree mix.  HUB = false: the row's update
+// follows in the same pass; HUB = true: rows are (b, h) slices of hub_src and the
+// sums go to s_hub[h].
 #ifndef FR_PI_UNROLL
 #define FR_PI_UNROLL 4
 #endif
 static constexpr int PI_UNROLL = FR_PI_UNROLL;
 #ifndef FR_PI_MINB
-#define FR_PI_MINB 1
+#define FR_PI_MINB 4  // 4 blocks x 8 warps per SM: <= 64 registers
 #endif
-// One 32-row tile (warp): the rows' compacted edge space split into 32 equal
-// contiguous chunks, one per lane (see k_pi_rows).  gather(j) returns z_j.
-template <bool HUB, typename G>
+template <bool HUB>
 __device__ __forceinline__ void pi_tile(const PiArgs &a, long long t, long long nrows, u32 *s_pre, u64 *s_lo,
-                                        double *s_acc, double &acc_block, G gather) {
+                                        double *s_acc, const double *__restrict__ z, double *zw, double c,
+                                        double &diff, double &nd) {
     constexpr u32 FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const long long r = t * 32 + lane;
+    const u32 *__restrict__ src = HUB ? a.hub_src : a.in_src;
     u64 lo = 0, deg = 0;
+    bool hub_row = false;
     if (r < nrows) {
         if (HUB) {
             lo = a.h_lo[r];
@@ -125,7 +172,17 @@ __device__ __forceinline__ void pi_tile(const PiArgs &a, long long t, long long 
             lo = a.in_off[r];
             deg = a.in_off[r + 1] - lo;
         }
-        if (deg > LONG_ROW) deg = 0;  // hub rows (short kernel) / long slices (k_pi_segs)
+        if (deg > LONG_ROW) {  // hub rows (short kernel) / long slices (k_pi_segs)
+            deg = 0;
+            hub_row = true;
+        }
+    }
+    // the update's operands are loaded now, in flight with the gathers
+    double xo = 0.0, wo = 0.0, vo = a.v_const;
+    if (!HUB && r < nrows && !hub_row) {
+        xo = a.x[r];
+        wo = a.inv[r];
+        if (a.v) vo = a.v[r];
     }
     u32 inc = (u32)deg;
 #pragma unroll
@@ -150,7 +207,7 @@ __device__ __forceinline__ void pi_tile(const PiArgs &a, long long t, long long 
         for (int step = 16; step >= 1; step >>= 1)
             if (s_pre[k + step] <= q) k += step;
         u32 rend = s_pre[k + 1];
-        u64 base = s_lo[k] - s_pre[k];  // in_src position of edge q' of row k: base + q'
+        u64 base = s_lo[k] - s_pre[k];  // src position of edge q' of row k: base + q'
         double acc = 0.0;
         // software pipeline: the column indices of the next batch are loaded
         // while the current batch's gathers are in flight (the load walk has
@@ -159,17 +216,17 @@ __device__ __forceinline__ void pi_tile(const PiArgs &a, long long t, long long 
         u32 lre = rend;
         u64 lbs = base;
         u32 lq = q;  // next edge whose index is loaded
-        auto load_batch = [&](u32 (&src)[PI_UNROLL]) {
+        auto load_batch = [&](u32 (&sv)[PI_UNROLL]) {
 #pragma unroll
             for (int j = 0; j < PI_UNROLL; j++) {
-                src[j] = 0;
+                sv[j] = 0;
                 if (lq < qe) {
                     while (lq >= lre) {
                         lk++;
                         lre = s_pre[lk + 1];
                         lbs = s_lo[lk] - s_pre[lk];
                     }
-                    src[j] = __ldg(a.in_src + lbs + lq);
+                    sv[j] = __ldg(src + lbs + lq);
                     lq++;
                 }
             }
@@ -179,7 +236,7 @@ __device__ __forceinline__ void pi_tile(const PiArgs &a, long long t, long long 
         while (q < qe) {
             double zv[PI_UNROLL];
 #pragma unroll
-            for (int j = 0; j < PI_UNROLL; j++) zv[j] = q + j < qe ? gather(srcA[j]) : 0.0;
+            for (int j = 0; j < PI_UNROLL; j++) zv[j] = q + j < qe ? z[srcA[j]] : 0.0;
             load_batch(srcB);
 #pragma unroll
             for (int j = 0; j < PI_UNROLL; j++) {
@@ -202,9 +259,11 @@ __device__ __forceinline__ void pi_tile(const PiArgs &a, long long t, long long 
     __syncwarp();
     if (r < nrows) {
         const double v = s_acc[lane];
-        if (!HUB) a.s[r] = v;  // 0 for hub rows: their (b, h) slices accumulate next
-        else if (v != 0.0) atomicAdd(a.s + a.hub_node[(u64)r % a.nhub], v);
-        acc_block += v;
+        if (HUB) {
+            if (v != 0.0) atomicAdd(a.s_hub + (u64)r % a.nhub, v);
+        } else if (!hub_row) {
+            pi_update_row(a, r, v, c, zw, xo, wo, vo, diff, nd);
+        }
     }
 }
 
@@ -227,8 +286,11 @@ __global__ void __launch_bounds__(PI_NT, FR_PI_MINB) k_pi_rows(PiArgs a) {
     u64 *next = a.ctl->seg_next[HUB ? 1 : 0];
     int seg = (int)(((long long)blockIdx.x * NW + w) % PI_SEGS), misses = 0;
     long long t = 0, t_end = 0;
-    double acc_block = 0.0;
-    const double *__restrict__ z = a.z;
+    const u64 it = a.ctl->iters;
+    const double c = a.ctl->c;
+    const double *__restrict__ z = z_rd(a, it);
+    double *zw = z_wr(a, it);
+    double diff = 0.0, nd = 0.0;
     for (;;) {
         if (t >= t_end) {
             bool got = false;
@@ -248,98 +310,69 @@ __global__ void __launch_bounds__(PI_NT, FR_PI_MINB) k_pi_rows(PiArgs a) {
             }
             if (!got) break;
         }
-        pi_tile<HUB>(a, t, nrows, s_pre[w], s_lo[w], s_acc[w], acc_block, [&](u32 j) { return z[j]; });
+        pi_tile<HUB>(a, t, nrows, s_pre[w], s_lo[w], s_acc[w], z, zw, c, diff, nd);
         t++;
     }
-    acc_block = block_sum<PI_NT>(acc_block, sm);
-    if (threadIdx.x == 0) a.part_s[(HUB ? 2 * a.nparts : 0) + blockIdx.x] = acc_block;
+    if (!HUB) {
+        diff = block_sum<PI_NT>(diff, sm);
+        nd = block_sum<PI_NT>(nd, sm);
+        if (threadIdx.x == 0) {
+            a.part_d[blockIdx.x] = diff;
+            a.part_nd[blockIdx.x] = nd;
+        }
+    }
 }
 
-// Warp per segment of a long row.
+// Warp per segment of a long (b, h) slice.
 __global__ void __launch_bounds__(PI_NT) k_pi_segs(PiArgs a) {
-    __shared__ double sm[PI_NT / 32];
     const int lane = threadIdx.x & 31;
-    double acc_block = 0.0;
+    const double *__restrict__ z = z_rd(a, a.ctl->iters);
     const long long nw = (long long)gridDim.x * (PI_NT / 32);
     for (long long q = blockIdx.x * (long long)(PI_NT / 32) + (threadIdx.x >> 5); q < a.nseg; q += nw) {
         const u64 lo = a.seg_lo[q], hi = a.seg_hi[q];
         double acc = 0.0;
-        for (u64 k = lo + lane; k < hi; k += 32) acc += a.z[__ldg(a.in_src + k)];
+        for (u64 k = lo + lane; k < hi; k += 32) acc += z[__ldg(a.hub_src + k)];
         acc = warp_sum(acc);
-        if (lane == 0) {
-            atomicAdd(a.s + a.seg_row[q], acc);
-            acc_block += acc;
-        }
-    }
-    acc_block = block_sum<PI_NT>(acc_block, sm);
-    if (threadIdx.x == 0) a.part_s[a.nparts + blockIdx.x] = acc_block;
-}
-
-__global__ void __launch_bounds__(PI_NT) k_pi_mass(PiArgs a) {
-    __shared__ double sm[PI_NT / 32];
-    double t = 0.0;
-    for (int p = threadIdx.x; p < 3 * a.nparts; p += PI_NT) t += a.part_s[p];
-    t = block_sum<PI_NT>(t, sm);
-    if (threadIdx.x == 0) {
-        const double ysum = a.d * t + (1.0 - a.d) * a.ctl->sum_v;
-        a.ctl->c = 1.0 - ysum;  // baseline.py:45 dangling mass back through v
+        if (lane == 0) atomicAdd(a.s_hub + a.seg_row[q], acc);
     }
 }
 
-// x, z, s, v, inv are distinct arrays: the restrict-qualified copies let the
-// compiler keep PI_UPD loads of independent nodes in flight (the loop was one
-// node at a time behind the stores before)
-static constexpr int PI_UPD = 4;
-__global__ void __launch_bounds__(PI_NT) k_pi_update(PiArgs a) {
+// The hub rows' update once every slice has been added (and s_hub cleared for
+// the next iteration).
+__global__ void __launch_bounds__(PI_NT) k_pi_hub_update(PiArgs a) {
     __shared__ double sm[PI_NT / 32];
+    const u64 it = a.ctl->iters;
     const double c = a.ctl->c;
-    const double *__restrict__ v = a.v;
-    const double *__restrict__ s = a.s;
-    const double *__restrict__ inv = a.inv;
-    double *__restrict__ x = a.x;
-    double *__restrict__ z = a.z;
-    double diff = 0.0;
-    const long long stride = (long long)gridDim.x * PI_NT;
-    long long i = blockIdx.x * (long long)PI_NT + threadIdx.x;
-    for (; i + (PI_UPD - 1) * stride < a.n; i += PI_UPD * stride) {
-        double vi[PI_UPD], si[PI_UPD], xi[PI_UPD], wi[PI_UPD];
-#pragma unroll
-        for (int u = 0; u < PI_UPD; u++) {
-            vi[u] = v[i + u * stride];
-            si[u] = s[i + u * stride];
-            xi[u] = x[i + u * stride];
-            wi[u] = inv[i + u * stride];
-        }
-#pragma unroll
-        for (int u = 0; u < PI_UPD; u++) {
-            double y = a.d * si[u] + (1.0 - a.d) * vi[u];
-            y += c * vi[u];
-            diff += fabs(y - xi[u]);
-            x[i + u * stride] = y;
-            z[i + u * stride] = y * wi[u];
-        }
-    }
-    for (; i < a.n; i += stride) {
-        const double vi = v[i];
-        double y = a.d * s[i] + (1.0 - a.d) * vi;
-        y += c * vi;
-        diff += fabs(y - x[i]);
-        x[i] = y;
-        z[i] = y * inv[i];
+    double *zw = z_wr(a, it);
+    double diff = 0.0, nd = 0.0;
+    for (long long h = blockIdx.x * (long long)PI_NT + threadIdx.x; h < a.nhub; h += (long long)gridDim.x * PI_NT) {
+        const double s = a.s_hub[h];
+        a.s_hub[h] = 0.0;
+        const u32 i = a.hub_node[h];
+        pi_update_row(a, i, s, c, zw, a.x[i], a.inv[i], a.v ? a.v[i] : a.v_const, diff, nd);
     }
     diff = block_sum<PI_NT>(diff, sm);
-    if (threadIdx.x == 0) a.part_d[blockIdx.x] = diff;
+    nd = block_sum<PI_NT>(nd, sm);
+    if (threadIdx.x == 0) {
+        a.part_d[a.nparts + blockIdx.x] = diff;
+        a.part_nd[a.nparts + blockIdx.x] = nd;
+    }
 }
 
 __global__ void __launch_bounds__(PI_NT) k_pi_check(PiArgs a) {
     __shared__ double sm[PI_NT / 32];
-    double t = 0.0;
-    for (int p = threadIdx.x; p < a.nparts; p += PI_NT) t += a.part_d[p];
+    double t = 0.0, nd = 0.0;
+    for (int p = threadIdx.x; p < a.nparts + a.hub_grid; p += PI_NT) {
+        t += a.part_d[p];
+        nd += a.part_nd[p];
+    }
     t = block_sum<PI_NT>(t, sm);
+    nd = block_sum<PI_NT>(nd, sm);
     reset_fronts(a.ctl);
     if (threadIdx.x == 0) {
         PiCtl *c = a.ctl;
         c->diff = t;
+        c->c = 1.0 - (a.d * nd + (1.0 - a.d) * c->sum_v);  // baseline.py:42 for the next iteration
         c->iters += 1;
         const bool done = t * (a.d / (1.0 - a.d)) <= a.target || (long long)c->iters >= a.max_iter;
         c->stop = done ? 1u : 0u;
@@ -352,10 +385,6 @@ __global__ void k_pi_inv(long long n, const u64 *__restrict__ off, double *__res
         const u64 d = off[i + 1] - off[i];
         inv[i] = d ? 1.0 / (double)d : 0.0;
     }
-}
-__global__ void k_fill(long long n, double v, double *x) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        x[i] = v;
 }
 __global__ void k_long_rows(long long n, const u64 *__restrict__ off, u32 *list, u32 *count) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -389,6 +418,18 @@ __global__ void k_hub_lo(const u32 *__restrict__ hub, u32 H, long long nb, const
         }
     }
 }
+// Block-major private copy of the hub rows' in-edges: slice r moves from
+// in_src[from[r], +cnt[r]) to hub_src[to[r], +cnt[r]) (warp per slice).
+__global__ void k_hub_copy(long long R, const u32 *__restrict__ in_src, const u64 *__restrict__ from,
+                           const u64 *__restrict__ to, const u32 *__restrict__ cnt, u32 *__restrict__ hub_src) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < R; r += nw) {
+        const u64 f = from[r], t = to[r];
+        const u32 c = cnt[r];
+        for (u32 k = lane; k < c; k += 32) hub_src[t + k] = in_src[f + k];
+    }
+}
 
 }  // namespace fr
 
@@ -406,7 +447,6 @@ struct fr_power {
     double target;
     long long max_iter;
     int grid;
-    int seg_grid;
 };
 
 static int add_node(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *dep, void *func, int grid, void **args) {
@@ -419,6 +459,8 @@ static int add_node(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t 
     return FR_OK;
 }
 
+// One iteration: short rows with their update, hub slices, long hub segments,
+// the hub rows' update, the stopping rule (and c of the next iteration).
 static int power_build_graph(fr_power *p) {
     if (p->exec) { cudaGraphExecDestroy(p->exec); p->exec = nullptr; }
     if (p->graph) { cudaGraphDestroy(p->graph); p->graph = nullptr; }
@@ -428,22 +470,22 @@ static int power_build_graph(fr_power *p) {
     p->a.target = p->target;
     p->a.max_iter = p->max_iter;
     void *args[] = {&p->a};
-    cudaGraphNode_t n_init, n_while;
+    cudaGraphNode_t n_init, n_start, n_while;
     FR_TRY(add_node(p->graph, &n_init, nullptr, (void *)k_pi_init, p->grid, args));
+    FR_TRY(add_node(p->graph, &n_start, &n_init, (void *)k_pi_start, 1, args));
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = p->a.cond;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
-    FR_CUDA(cudaGraphAddNode(&n_while, p->graph, &n_init, 1, &cp));
+    FR_CUDA(cudaGraphAddNode(&n_while, p->graph, &n_start, 1, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    cudaGraphNode_t n1, n1h, n2, n3, n4, n5;
+    cudaGraphNode_t n1, n1h, n2, n3, n4;
     FR_TRY(add_node(body, &n1, nullptr, (void *)k_pi_rows<false>, p->grid, args));
     FR_TRY(add_node(body, &n1h, &n1, (void *)k_pi_rows<true>, p->grid, args));
     FR_TRY(add_node(body, &n2, &n1h, (void *)k_pi_segs, p->grid, args));
-    FR_TRY(add_node(body, &n3, &n2, (void *)k_pi_mass, 1, args));
-    FR_TRY(add_node(body, &n4, &n3, (void *)k_pi_update, p->grid, args));
-    FR_TRY(add_node(body, &n5, &n4, (void *)k_pi_check, 1, args));
+    FR_TRY(add_node(body, &n3, &n2, (void *)k_pi_hub_update, p->a.hub_grid, args));
+    FR_TRY(add_node(body, &n4, &n3, (void *)k_pi_check, 1, args));
     FR_CUDA(cudaGraphInstantiate(&p->exec, p->graph, 0));
     return FR_OK;
 }
@@ -484,39 +526,6 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
         p->grid = di.sms * 8;
         a.nparts = p->grid;
         cudaError_t e;
-        // inv, v, x, z, s + partials
-        if ((e = cudaMalloc(&p->buf, sizeof(double) * (5 * (size_t)n + 4 * (size_t)p->grid))) != cudaSuccess ||
-            (e = cudaMalloc(&p->ctl, sizeof(PiCtl))) != cudaSuccess) {
-            rc = cuda_fail(e, "cudaMalloc(power)", __FILE__, __LINE__);
-            break;
-        }
-        double *inv = p->buf, *v = inv + n;
-        a.inv = inv;
-        a.v = v;
-        a.x = v + n;
-        a.z = a.x + n;
-        a.s = a.z + n;
-        a.part_s = a.s + n;           // 3 * grid (short rows, segments, hub slices)
-        a.part_d = a.part_s + 3 * p->grid;
-        a.ctl = p->ctl;
-        k_pi_inv<<<p->grid, PI_NT, 0, st>>>(n, reinterpret_cast<const u64 *>(d_out_offsets), inv);
-        if (d_teleport) {
-            if ((e = cudaMemcpyAsync(v, d_teleport, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st)) !=
-                cudaSuccess) {
-                rc = cuda_fail(e, "copy teleport", __FILE__, __LINE__);
-                break;
-            }
-        } else {
-            k_fill<<<p->grid, PI_NT, 0, st>>>(n, 1.0 / (double)n, v);
-        }
-        double sum_v = 0.0;
-        if ((rc = fr_abs_sum(n, v, 0, &sum_v, st)) != FR_OK) break;
-        PiCtl hc = {};
-        hc.sum_v = sum_v;
-        if ((e = cudaMemcpyAsync(p->ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st)) != cudaSuccess) {
-            rc = cuda_fail(e, "ctl", __FILE__, __LINE__);
-            break;
-        }
         // hub rows: in-degree > LONG_ROW
         Scratch scratch(st);
         u32 *d_list, *d_cnt;
@@ -527,44 +536,110 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
         u32 nlong = 0;
         cudaMemcpyAsync(&nlong, d_cnt, sizeof(u32), cudaMemcpyDeviceToHost, st);
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "long rows", __FILE__, __LINE__); break; }
-        // hub rows regrouped by source block (k_pi_rows<true>, k_pi_segs)
+        a.nhub = nlong;
+        a.hub_grid = (int)std::max<long long>(1, std::min<long long>(p->grid, ((long long)nlong + PI_NT - 1) / PI_NT));
+        // inv, x, z (two buffers), s_hub [, v] + partials (|y - x| and non-dangling sums)
+        const size_t nv = d_teleport ? (size_t)n : 0;
+        const size_t parts = (size_t)(p->grid + a.hub_grid);
+        if ((e = cudaMalloc(&p->buf, sizeof(double) * (4 * (size_t)n + nlong + nv + 2 * parts))) != cudaSuccess ||
+            (e = cudaMalloc(&p->ctl, sizeof(PiCtl))) != cudaSuccess) {
+            rc = cuda_fail(e, "cudaMalloc(power)", __FILE__, __LINE__);
+            break;
+        }
+        double *inv = p->buf;
+        a.inv = inv;
+        a.x = inv + n;
+        a.zb[0] = a.x + n;
+        a.zb[1] = a.zb[0] + n;
+        a.s_hub = a.zb[1] + n;
+        double *v = a.s_hub + nlong;
+        a.part_d = v + nv;
+        a.part_nd = a.part_d + parts;
+        a.ctl = p->ctl;
+        k_pi_inv<<<p->grid, PI_NT, 0, st>>>(n, reinterpret_cast<const u64 *>(d_out_offsets), inv);
+        double sum_v = 1.0;
+        if (d_teleport) {
+            if ((e = cudaMemcpyAsync(v, d_teleport, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st)) !=
+                cudaSuccess) {
+                rc = cuda_fail(e, "copy teleport", __FILE__, __LINE__);
+                break;
+            }
+            a.v = v;
+            if ((rc = fr_abs_sum(n, v, 0, &sum_v, st)) != FR_OK) break;
+        } else {
+            // uniform teleport: v_i = 1/n is not stored (one 8 B read less per row)
+            a.v = nullptr;
+            a.v_const = 1.0 / (double)n;
+            sum_v = (double)n * a.v_const;
+        }
+        PiCtl hc = {};
+        hc.sum_v = sum_v;
+        if ((e = cudaMemcpyAsync(p->ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+            rc = cuda_fail(e, "ctl", __FILE__, __LINE__);
+            break;
+        }
+        // hub rows regrouped by source block into a private block-major copy
         std::vector<u64> seg_row, seg_lo, seg_hi;
         const long long nb = (n + (1ll << PI_SB) - 1) >> PI_SB;
-        a.nhub = nlong;
         a.h_rows = nlong ? nb * (long long)nlong : 0;
         if (nlong) {
             const size_t R = (size_t)a.h_rows;
-            if ((e = cudaMalloc(&p->hubbuf, sizeof(u32) * ((size_t)nlong + R) + sizeof(u64) * R + 16)) !=
-                cudaSuccess) {
-                rc = cuda_fail(e, "cudaMalloc(hub slices)", __FILE__, __LINE__);
-                break;
+            u64 *d_from, *d_to;
+            if ((rc = scratch.alloc(&d_from, R)) != FR_OK) break;
+            if ((rc = scratch.alloc(&d_to, R)) != FR_OK) break;
+            std::vector<u32> cnt(R), hubs(nlong);
+            u64 *h_lo;
+            u32 *h_cnt, *hub;
+            {
+                // counts first (they size the copy)
+                u32 *d_hub, *d_hcnt;
+                if ((rc = scratch.alloc(&d_hub, nlong)) != FR_OK) break;
+                if ((rc = scratch.alloc(&d_hcnt, R)) != FR_OK) break;
+                cudaMemcpyAsync(d_hub, d_list, sizeof(u32) * nlong, cudaMemcpyDeviceToDevice, st);
+                cudaMemsetAsync(d_hcnt, 0, sizeof(u32) * R, st);
+                k_hub_count<<<p->grid, PI_NT, 0, st>>>(d_hub, nlong, a.in_off, a.in_src, d_hcnt);
+                k_hub_lo<<<(nlong + 255) / 256, 256, 0, st>>>(d_hub, nlong, nb, a.in_off, d_hcnt, d_from);
+                cudaMemcpyAsync(cnt.data(), d_hcnt, sizeof(u32) * R, cudaMemcpyDeviceToHost, st);
+                cudaMemcpyAsync(hubs.data(), d_hub, sizeof(u32) * nlong, cudaMemcpyDeviceToHost, st);
+                if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "hub slices", __FILE__, __LINE__); break; }
+                // hub_src layout: the short slices in (b, h) order, then the long ones
+                std::vector<u64> to(R);
+                u64 pos = 0;
+                for (size_t r = 0; r < R; r++)
+                    if (cnt[r] <= LONG_ROW) { to[r] = pos; pos += cnt[r]; }
+                const u64 es = pos;
+                for (size_t r = 0; r < R; r++)
+                    if (cnt[r] > LONG_ROW) {
+                        to[r] = pos;
+                        for (u64 b = pos; b < pos + cnt[r]; b += SEG) {
+                            seg_row.push_back(r % nlong);
+                            seg_lo.push_back(b);
+                            seg_hi.push_back(std::min<u64>(pos + cnt[r], b + SEG));
+                        }
+                        pos += cnt[r];
+                    }
+                (void)es;
+                if ((e = cudaMalloc(&p->hubbuf, sizeof(u64) * R + sizeof(u32) * (R + nlong + pos) + 16)) !=
+                    cudaSuccess) {
+                    rc = cuda_fail(e, "cudaMalloc(hub slices)", __FILE__, __LINE__);
+                    break;
+                }
+                h_lo = (u64 *)p->hubbuf;
+                h_cnt = (u32 *)(h_lo + R);
+                hub = h_cnt + R;
+                u32 *hub_src = hub + nlong;
+                cudaMemcpyAsync(d_to, to.data(), sizeof(u64) * R, cudaMemcpyHostToDevice, st);
+                k_hub_copy<<<p->grid, PI_NT, 0, st>>>((long long)R, a.in_src, d_from, d_to, d_hcnt, hub_src);
+                cudaMemcpyAsync(h_lo, d_to, sizeof(u64) * R, cudaMemcpyDeviceToDevice, st);
+                cudaMemcpyAsync(h_cnt, d_hcnt, sizeof(u32) * R, cudaMemcpyDeviceToDevice, st);
+                cudaMemcpyAsync(hub, d_hub, sizeof(u32) * nlong, cudaMemcpyDeviceToDevice, st);
+                if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "hub copy", __FILE__, __LINE__); break; }
+                a.hub_src = hub_src;
             }
-            u64 *h_lo = (u64 *)p->hubbuf;
-            u32 *h_cnt = (u32 *)(h_lo + R);
-            u32 *hub = h_cnt + R;
-            cudaMemcpyAsync(hub, d_list, sizeof(u32) * nlong, cudaMemcpyDeviceToDevice, st);
-            cudaMemsetAsync(h_cnt, 0, sizeof(u32) * R, st);
-            k_hub_count<<<p->grid, PI_NT, 0, st>>>(hub, nlong, a.in_off, a.in_src, h_cnt);
-            k_hub_lo<<<(nlong + 255) / 256, 256, 0, st>>>(hub, nlong, nb, a.in_off, h_cnt, h_lo);
+            if (rc != FR_OK) break;
             a.h_lo = h_lo;
             a.h_cnt = h_cnt;
             a.hub_node = hub;
-            // slices longer than LONG_ROW become warp segments (host list, once)
-            std::vector<u32> cnt(R), hubs(nlong);
-            std::vector<u64> los(R);
-            cudaMemcpyAsync(cnt.data(), h_cnt, sizeof(u32) * R, cudaMemcpyDeviceToHost, st);
-            cudaMemcpyAsync(los.data(), h_lo, sizeof(u64) * R, cudaMemcpyDeviceToHost, st);
-            cudaMemcpyAsync(hubs.data(), hub, sizeof(u32) * nlong, cudaMemcpyDeviceToHost, st);
-            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "hub slices", __FILE__, __LINE__); break; }
-            for (size_t r = 0; r < R; r++) {
-                if (cnt[r] <= LONG_ROW) continue;
-                const u64 lo = los[r], hi = lo + cnt[r];
-                for (u64 b = lo; b < hi; b += SEG) {
-                    seg_row.push_back(hubs[r % nlong]);
-                    seg_lo.push_back(b);
-                    seg_hi.push_back(std::min(hi, b + SEG));
-                }
-            }
         }
         a.nseg = (long long)seg_row.size();
         if ((e = cudaMalloc(&p->segbuf, sizeof(u64) * (3 * seg_row.size() + 3))) != cudaSuccess) {
@@ -591,9 +666,9 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
 
 // The same iterations launched one by one from the host with CUDA events around
 // each kernel class: the roofline report of bench.py, not the timed path.
-// h_ms[0] = short rows (k_pi_rows<false>), h_ms[1] = hub rows by source block
-// (k_pi_rows<true> + k_pi_segs), h_ms[2] = the rest (dangling mass, update,
-// check), summed over the iterations.
+// h_ms[0] = short rows with their update (k_pi_rows<false>), h_ms[1] = hub slices
+// by source block (k_pi_rows<true>), h_ms[2] = long hub slices (k_pi_segs), h_ms[3]
+// = the rest (hub rows' update, check), summed over the iterations.
 extern "C" int fr_power_run_profiled(fr_power *p, double target_error, int64_t max_iterations, double *d_x,
                                      int64_t *h_iterations, double *h_ms, void *stream) {
     if (!p || !(target_error > 0.0) || !d_x || !h_ms) {
@@ -605,33 +680,34 @@ extern "C" int fr_power_run_profiled(fr_power *p, double target_error, int64_t m
     a.in_graph = 0;
     a.target = target_error;
     a.max_iter = max_iterations > 0 ? max_iterations : 1000000;
-    cudaEvent_t ev[4];
-    for (int i = 0; i < 4; i++) FR_CUDA(cudaEventCreate(&ev[i]));
-    h_ms[0] = h_ms[1] = h_ms[2] = 0.0;
+    cudaEvent_t ev[5];
+    for (int i = 0; i < 5; i++) FR_CUDA(cudaEventCreate(&ev[i]));
+    h_ms[0] = h_ms[1] = h_ms[2] = h_ms[3] = 0.0;
     k_pi_init<<<p->grid, PI_NT, 0, st>>>(a);
+    k_pi_start<<<1, PI_NT, 0, st>>>(a);
     PiCtl hc = {};
     for (;;) {
         FR_CUDA(cudaEventRecord(ev[0], st));
         k_pi_rows<false><<<p->grid, PI_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[1], st));
         k_pi_rows<true><<<p->grid, PI_NT, 0, st>>>(a);
-        k_pi_segs<<<p->grid, PI_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[2], st));
-        k_pi_mass<<<1, PI_NT, 0, st>>>(a);
-        k_pi_update<<<p->grid, PI_NT, 0, st>>>(a);
-        k_pi_check<<<1, PI_NT, 0, st>>>(a);
+        k_pi_segs<<<p->grid, PI_NT, 0, st>>>(a);
         FR_CUDA(cudaEventRecord(ev[3], st));
+        k_pi_hub_update<<<a.hub_grid, PI_NT, 0, st>>>(a);
+        k_pi_check<<<1, PI_NT, 0, st>>>(a);
+        FR_CUDA(cudaEventRecord(ev[4], st));
         FR_CUDA(cudaGetLastError());
         FR_CUDA(cudaMemcpyAsync(&hc, p->ctl, sizeof(hc), cudaMemcpyDeviceToHost, st));
         FR_CUDA(cudaStreamSynchronize(st));
-        for (int k = 0; k < 3; k++) {
+        for (int k = 0; k < 4; k++) {
             float t = 0.f;
             FR_CUDA(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
             h_ms[k] += t;
         }
         if (hc.stop) break;
     }
-    for (int i = 0; i < 4; i++) cudaEventDestroy(ev[i]);
+    for (int i = 0; i < 5; i++) cudaEventDestroy(ev[i]);
     FR_CUDA(cudaMemcpyAsync(d_x, p->a.x, sizeof(double) * (size_t)p->n, cudaMemcpyDeviceToDevice, st));
     FR_CUDA(cudaStreamSynchronize(st));
     if (h_iterations) *h_iterations = (int64_t)hc.iters;
