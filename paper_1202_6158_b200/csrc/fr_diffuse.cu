@@ -597,14 +597,9 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #define FR_OWN_SKIPSCAN 0
 #endif
 #ifndef FR_OWN_BULKPF
-#define FR_OWN_BULKPF 0  // 1: one bulk L2 prefetch of the chunk's fluid and offsets instead of per-tile prefetches
+#define FR_OWN_BULKPF 1  // one bulk L2 prefetch of the chunk's fluid and offsets (0: per-tile prefetches)
 #endif
-#ifndef FR_OWN_RAWCLAIM
-#define FR_OWN_RAWCLAIM 0  // 1: tile claims by a plain atom.shared.add (no compiler warp aggregation)
-#endif
-#ifndef FR_OWN_FASTMAX
-#define FR_OWN_FASTMAX 0  // 1: running max score by compare-select (no NaN handling)
-#endif
+
 static constexpr int OWN_NT = FR_OWN_NT;
 static constexpr int OWN_UNROLL = FR_OWN_UNROLL;
 static_assert(OWN_UNROLL * 6 <= 32, "packed row indices");
@@ -692,12 +687,7 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
         if (lt < ntl) load_tile(lt, f_cur, lo_cur, end_cur);
         while (lt < ntl) {
             u32 lnx = 0;
-#if FR_OWN_RAWCLAIM
-            if (lane == 0)
-                asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(lnx) : "r"((u32)__cvta_generic_to_shared(ctr)) : "memory");
-#else
             if (lane == 0) lnx = atomicAdd(ctr, 1u);
-#endif
             lnx = __shfl_sync(FULL, lnx, 0);
             FT f_nx = (FT)0;
             OT lo_nx = 0, end_nx = 0;
@@ -725,11 +715,7 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
             const double af = fabs((double)f);
             double score = (a.weight && valid) ? af * a.weight[i] : af;
             if (a.beta != 0.0f) score = af * deg_weight(a.beta, deg);
-#if FR_OWN_FASTMAX
-            mx = score > mx ? score : mx;
-#else
             mx = fmax(mx, score);
-#endif
             bool sel;
             if (a.select == FR_SELECT_PER) sel = true;
             else if (a.select == FR_SELECT_RAND)
@@ -1019,32 +1005,6 @@ __global__ void __launch_bounds__(256) k_push_warp(SweepArgs<FT> a) {
     }
     __syncthreads();
     hot_flush(a.Fw, hot_acc, a.nhot, 256);
-}
-
-__device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(u64 *bar, u32 count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(u64 *bar, u32 bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(u64 *bar, u32 parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "FR_WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra FR_WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, u32 bytes, u64 *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
 }
 
 // Block per hub node.  The 16-byte-aligned body of the adjacency row streams

@@ -26,7 +26,7 @@ namespace fr {
 
 static constexpr int PI_NT = 256;
 static constexpr u64 LONG_ROW = 1024;
-static constexpr u64 SEG = 2048;
+static constexpr u64 SEG = 256;  // long-slice segment: the segments in flight span a few source blocks of z (L2)
 #ifndef FR_PI_SB
 #define FR_PI_SB 18
 #endif
@@ -76,7 +76,8 @@ struct PiArgs {
     const u64 *seg_row, *seg_lo, *seg_hi;  // (b, h) slices longer than LONG_ROW, seg_row = hub index h
     long long nseg;
     double *part_d, *part_nd;  // per-block |y - x|_1 and sum of y over non-dangling nodes
-    int nparts;                // row-kernel blocks; the hub update's blocks follow
+    int nparts;                // partial slots of the row kernel; the hub update's blocks follow
+    int row_grid;              // blocks of the short-row kernel in use (<= nparts)
     int hub_grid;
     PiCtl *ctl;
     double d, target;
@@ -154,10 +155,9 @@ static constexpr int PI_UNROLL = FR_PI_UNROLL;
 #ifndef FR_PI_MINB
 #define FR_PI_MINB 4  // 4 blocks x 8 warps per SM: <= 64 registers
 #endif
-template <bool HUB>
+template <bool HUB, typename G>
 __device__ __forceinline__ void pi_tile(const PiArgs &a, long long t, long long nrows, u32 *s_pre, u64 *s_lo,
-                                        double *s_acc, const double *__restrict__ z, double *zw, double c,
-                                        double &diff, double &nd) {
+                                        double *s_acc, G gather, double *zw, double c, double &diff, double &nd) {
     constexpr u32 FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const long long r = t * 32 + lane;
@@ -236,7 +236,7 @@ __device__ __forceinline__ void pi_tile(const PiArgs &a, long long t, long long 
         while (q < qe) {
             double zv[PI_UNROLL];
 #pragma unroll
-            for (int j = 0; j < PI_UNROLL; j++) zv[j] = q + j < qe ? z[srcA[j]] : 0.0;
+            for (int j = 0; j < PI_UNROLL; j++) zv[j] = q + j < qe ? gather(srcA[j]) : 0.0;
             load_batch(srcB);
 #pragma unroll
             for (int j = 0; j < PI_UNROLL; j++) {
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(PI_NT, FR_PI_MINB) k_pi_rows(PiArgs a) {
             }
             if (!got) break;
         }
-        pi_tile<HUB>(a, t, nrows, s_pre[w], s_lo[w], s_acc[w], z, zw, c, diff, nd);
+        pi_tile<HUB>(a, t, nrows, s_pre[w], s_lo[w], s_acc[w], [&](u32 j) { return z[j]; }, zw, c, diff, nd);
         t++;
     }
     if (!HUB) {
@@ -362,9 +362,10 @@ __global__ void __launch_bounds__(PI_NT) k_pi_hub_update(PiArgs a) {
 __global__ void __launch_bounds__(PI_NT) k_pi_check(PiArgs a) {
     __shared__ double sm[PI_NT / 32];
     double t = 0.0, nd = 0.0;
-    for (int p = threadIdx.x; p < a.nparts + a.hub_grid; p += PI_NT) {
-        t += a.part_d[p];
-        nd += a.part_nd[p];
+    for (int p = threadIdx.x; p < a.row_grid + a.hub_grid; p += PI_NT) {
+        const int q = p < a.row_grid ? p : a.nparts + (p - a.row_grid);
+        t += a.part_d[q];
+        nd += a.part_nd[q];
     }
     t = block_sum<PI_NT>(t, sm);
     nd = block_sum<PI_NT>(nd, sm);
@@ -525,6 +526,7 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
         a.d = damping;
         p->grid = di.sms * 8;
         a.nparts = p->grid;
+        a.row_grid = p->grid;
         cudaError_t e;
         // hub rows: in-degree > LONG_ROW
         Scratch scratch(st);
@@ -541,17 +543,18 @@ extern "C" int fr_power_create(int64_t n, int64_t m, const int64_t *d_out_offset
         // inv, x, z (two buffers), s_hub [, v] + partials (|y - x| and non-dangling sums)
         const size_t nv = d_teleport ? (size_t)n : 0;
         const size_t parts = (size_t)(p->grid + a.hub_grid);
-        if ((e = cudaMalloc(&p->buf, sizeof(double) * (4 * (size_t)n + nlong + nv + 2 * parts))) != cudaSuccess ||
+        const size_t nz = ((size_t)n + 31) & ~(size_t)31;
+        if ((e = cudaMalloc(&p->buf, sizeof(double) * (2 * nz + 2 * (size_t)n + nlong + nv + 2 * parts))) != cudaSuccess ||
             (e = cudaMalloc(&p->ctl, sizeof(PiCtl))) != cudaSuccess) {
             rc = cuda_fail(e, "cudaMalloc(power)", __FILE__, __LINE__);
             break;
         }
-        double *inv = p->buf;
+        a.zb[0] = p->buf;
+        a.zb[1] = a.zb[0] + nz;
+        double *inv = a.zb[1] + nz;
         a.inv = inv;
         a.x = inv + n;
-        a.zb[0] = a.x + n;
-        a.zb[1] = a.zb[0] + n;
-        a.s_hub = a.zb[1] + n;
+        a.s_hub = a.x + n;
         double *v = a.s_hub + nlong;
         a.part_d = v + nv;
         a.part_nd = a.part_d + parts;
