@@ -260,6 +260,13 @@ int fr_ppr_create(int64_t n, int64_t m, const int64_t *d_offsets, const uint32_t
  * diffusions = row visits, elementary_steps = edge visits, hub_edges = column
  * values scattered (one red.add each; zero pushes are skipped). */
 int fr_ppr_run(fr_ppr *p, void *stream, fr_solve_stats *h_stats, double *h_col_residual);
+/* Pull formulation (no atomics, bit-reproducible): the selected rows' pushes are
+ * written once and every node sums those of its selected parents over the
+ * transposed CSR (d_in_offsets int64[n+1], d_in_sources uint32[m], graph.py
+ * to_matrix(); the arrays must stay valid while the handle is used).  Jacobi
+ * within a sweep, so more sweeps than the default push (red.add scatter); the
+ * same fixed point per column. */
+int fr_ppr_set_pull(fr_ppr *p, const int64_t *d_in_offsets, const uint32_t *d_in_sources);
 int fr_ppr_destroy(fr_ppr *p);
 /* rank[:, c] = history[:, c] / sum |history[:, c]|. */
 int fr_ppr_normalize(int64_t n, int32_t B, const double *d_history, double *d_rank, void *stream);

@@ -91,6 +91,7 @@ SIGNATURES = {
     "fr_ppr_init": (ctypes.c_int, [_I64, _I32, _P, _I32, _F64, _P, _P, _P]),
     "fr_ppr_create": (ctypes.c_int, [_I64, _I64, _P, _P, _I32, _P, _P, _P, _P, _P]),
     "fr_ppr_run": (ctypes.c_int, [_P, _P, _P, _P]),
+    "fr_ppr_set_pull": (ctypes.c_int, [_P, _P, _P]),
     "fr_ppr_destroy": (ctypes.c_int, [_P]),
     "fr_ppr_normalize": (ctypes.c_int, [_I64, _I32, _P, _P, _P]),
 }

@@ -7,9 +7,22 @@
 // rule is the scalar solver's threshold sweep applied to the row maximum over
 // the columns that are still active, and column c stops (freezes: no more
 // pushes) once its residual R_c <= target*(1-d) is confirmed by an exact sum.
+//
+// Two formulations of a sweep (the same fixed point; parity is checked per column):
+//   push (k_ppr_sweep): a selected row scatters its B-wide push into each child
+//     with red.global.add -- every edge visit is B fp64 reductions in L2;
+//   pull (fr_ppr_set_pull; k_ppr_take + k_ppr_pull): the selected rows are taken
+//     and their pushes d*f/deg written once to a row buffer (sent) with a
+//     selection bitmap; then every node sums the sent rows of its selected
+//     parents over the transposed CSR into its own fluid row (plain loads and
+//     stores, no atomics: the 64-wide scatter was bound by the L2 reduction
+//     units, ~2e11 fp64 adds/s), and keeps its exact row maximum (rmax), so the
+//     next take reads 8 B per row instead of the row.  The pull is Jacobi within
+//     a sweep (a push reaches its child in the next sweep).
 #include <math.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "fr_common.cuh"
 
@@ -24,6 +37,8 @@ static constexpr int PP_NT = 256;
 #endif
 static constexpr int PP_SEGS = FR_PP_SEGS;
 static constexpr int PP_CHUNK = FR_PP_CHUNK;  // consecutive nodes per reservation (one warp per node)
+static constexpr u64 PULL_LONG = 1024;  // pull: rows with more parents are split into segments
+static constexpr u64 PULL_SEG = 2048;   // parents per segment
 
 struct PprCtl {
     double theta;
@@ -43,6 +58,20 @@ struct PprArgs {
     const u64 *off;
     const u32 *tgt;
     PprCtl *ctl;
+    // pull formulation (null in_off: push)
+    const u64 *in_off;
+    const u32 *in_src;
+    double *sent;        // [n][B] push values d*f/deg of the rows taken this sweep
+    u32 *selbits;        // [ceil(n/32)] rows taken this sweep that have children
+    double *rmax;        // [n] exact max_c |F[i][c]| over all columns
+    double *part_max2;   // [2 grid] max of the rows updated by the pull (short rows, hub rows)
+    // rows with more than PULL_LONG parents: summed by 2048-parent segments into
+    // per-segment partial rows, then added per hub in a fixed order
+    const u32 *hub_node;  // [nhub]
+    const u32 *hub_seg;   // [nhub + 1] first segment of each hub
+    const u64 *seg_lo, *seg_hi;  // [nseg] in_src range of each segment
+    double *seg_acc;      // [nseg][B]
+    u32 nhub, nseg;
     double *part_abs;    // [grid][64]
     double *part_max;    // [grid]
     u64 *part_sel, *part_steps, *part_push;
@@ -163,6 +192,226 @@ __global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
     }
 }
 
+// Pull formulation, take: warp per tile of 32 rows (grid-stride).  A row whose
+// exact maximum (rmax) reaches theta is read; it diffuses when its maximum over
+// the active columns does: F row -> 0, H += f, sent row = f*d/deg (0 in frozen
+// columns), its bit set; the tile's bitmap word is written whole every sweep.
+__global__ void __launch_bounds__(PP_NT) k_ppr_take(PprArgs a) {
+    __shared__ double s_abs[PP_NT / 32][64];
+    __shared__ double s_red[PP_NT / 32];
+    __shared__ u64 s_red64[PP_NT / 32];
+    constexpr u32 FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    PprCtl *c = a.ctl;
+    const double theta = c->theta;
+    const u64 active = c->active;
+    const int B = a.B;
+    const bool own0 = lane < B && ((active >> lane) & 1ull);
+    const bool own1 = lane + 32 < B && ((active >> (lane + 32)) & 1ull);
+    const bool col0 = lane < B, col1 = lane + 32 < B;
+    double ab0 = 0.0, ab1 = 0.0, mx = 0.0;
+    u64 nsel = 0, steps = 0, npush = 0;
+    const long long ntiles = (a.n + 31) / 32;
+    for (long long tl = blockIdx.x * (long long)(PP_NT / 32) + wid; tl < ntiles;
+         tl += (long long)gridDim.x * (PP_NT / 32)) {
+        const long long i0 = tl * 32, ti = i0 + lane;
+        const bool v = ti < a.n;
+        const double r = v ? a.rmax[ti] : 0.0;
+        const bool cand = r >= theta && r > 0.0;
+        if (!cand) mx = fmax(mx, r);
+        u32 cm = __ballot_sync(FULL, cand);
+        u32 bits = 0;
+        while (cm) {
+            const int j = __ffs(cm) - 1;
+            cm &= cm - 1;
+            const long long i = i0 + j;
+            double *Fi = a.F + (size_t)i * B;
+            const double f0 = own0 ? Fi[lane] : 0.0;
+            const double f1 = own1 ? Fi[lane + 32] : 0.0;
+            const double rowmax = warp_max_d(fmax(fabs(f0), fabs(f1)));  // active columns
+            if (!(rowmax >= theta && rowmax > 0.0)) {
+                // frozen columns hold the rest of rmax: keep the active maximum
+                mx = fmax(mx, rowmax);
+                if (lane == 0) a.rmax[i] = rowmax;
+                continue;
+            }
+            const u64 lo = a.off[i], hi = a.off[i + 1];
+            const u32 deg = (u32)(hi - lo);
+            double *Hi = a.H + (size_t)i * B;
+            if (own0) {
+                Fi[lane] = 0.0;
+                Hi[lane] += f0;
+            }
+            if (own1) {
+                Fi[lane + 32] = 0.0;
+                Hi[lane + 32] += f1;
+            }
+            if (lane == 0) {
+                a.rmax[i] = 0.0;  // the frozen columns are not searched again (their fluid stays)
+                nsel++;
+            }
+            if (deg == 0) {
+                ab0 += fabs(f0);
+                ab1 += fabs(f1);
+                continue;
+            }
+            ab0 += fabs(f0) * (1.0 - a.d);
+            ab1 += fabs(f1) * (1.0 - a.d);
+            if (lane == 0) steps += deg;
+            const double w = a.d / (double)deg;
+            const double p0 = f0 * w, p1 = f1 * w;  // sent*(d/deg), engine.py:321
+            npush += (u64)deg * ((own0 && p0 != 0.0) + (own1 && p1 != 0.0));
+            double *Si = a.sent + (size_t)i * B;
+            if (col0) Si[lane] = p0;
+            if (col1) Si[lane + 32] = p1;
+            bits |= 1u << j;
+        }
+        if (lane == 0 && i0 < a.n) a.selbits[tl] = bits;
+    }
+    s_abs[wid][lane] = ab0;
+    s_abs[wid][lane + 32] = ab1;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        double t = 0.0;
+        for (int w = 0; w < PP_NT / 32; w++) t += s_abs[w][threadIdx.x];
+        a.part_abs[(size_t)blockIdx.x * 64 + threadIdx.x] = t;
+    }
+    const double bmx = block_max<PP_NT>(mx, s_red);
+    const u64 bsel = block_sum_u64<PP_NT>(nsel, s_red64);
+    const u64 bst = block_sum_u64<PP_NT>(steps, s_red64);
+    const u64 bpu = block_sum_u64<PP_NT>(npush, s_red64);
+    if (threadIdx.x == 0) {
+        a.part_max[blockIdx.x] = bmx;
+        a.part_sel[blockIdx.x] = bsel;
+        a.part_steps[blockIdx.x] = bst;
+        a.part_push[blockIdx.x] = bpu;
+    }
+}
+
+// Sum of the sent rows of the selected parents in in_src[lo, hi) (warp; lanes
+// hold columns lane and lane + 32); returns whether any parent was selected.
+__device__ __forceinline__ bool pull_range(const PprArgs &a, u64 lo, u64 hi, bool col0, bool col1, double &acc0,
+                                           double &acc1) {
+    constexpr u32 FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int B = a.B;
+    bool any = false;
+    for (u64 k0 = lo; k0 < hi; k0 += 32) {
+        const bool v = k0 + lane < hi;
+        const u32 j = v ? __ldg(a.in_src + k0 + lane) : 0u;
+        const bool sel = v && ((__ldg(a.selbits + (j >> 5)) >> (j & 31)) & 1u);
+        u32 sm = __ballot_sync(FULL, sel);
+        any |= sm != 0;
+        // two parents per step: their four 256 B loads in flight together
+        while (sm) {
+            const int b0 = __ffs(sm) - 1;
+            sm &= sm - 1;
+            const u32 j0 = __shfl_sync(FULL, j, b0);
+            int b1 = -1;
+            if (sm) {
+                b1 = __ffs(sm) - 1;
+                sm &= sm - 1;
+            }
+            const u32 j1 = __shfl_sync(FULL, j, b1 < 0 ? b0 : b1);
+            const double *S0 = a.sent + (size_t)j0 * B;
+            const double *S1 = a.sent + (size_t)j1 * B;
+            const double x0 = col0 ? S0[lane] : 0.0, x1 = col1 ? S0[lane + 32] : 0.0;
+            const double y0 = (col0 && b1 >= 0) ? S1[lane] : 0.0, y1 = (col1 && b1 >= 0) ? S1[lane + 32] : 0.0;
+            acc0 += x0;
+            acc1 += x1;
+            acc0 += y0;
+            acc1 += y1;
+        }
+    }
+    return any;
+}
+
+// F row i += (acc0, acc1); its new exact maximum over the active columns
+__device__ __forceinline__ double pull_apply(const PprArgs &a, long long i, bool col0, bool col1, bool own0, bool own1,
+                                             double acc0, double acc1) {
+    const int lane = threadIdx.x & 31;
+    double *Fi = a.F + (size_t)i * a.B;
+    double f0 = 0.0, f1 = 0.0;
+    if (col0) {
+        f0 = Fi[lane] + acc0;
+        Fi[lane] = f0;
+    }
+    if (col1) {
+        f1 = Fi[lane + 32] + acc1;
+        Fi[lane + 32] = f1;
+    }
+    const double rm = warp_max_d(fmax(own0 ? fabs(f0) : 0.0, own1 ? fabs(f1) : 0.0));
+    if (lane == 0 && a.rmax) a.rmax[i] = rm;
+    return rm;
+}
+
+// Pull: warp per node, nodes in order (grid-stride: the warps in flight cover a
+// narrow id window, so the sent rows of the local parents stay in L2).  The
+// node's parents are tested against the bitmap 32 at a time; each selected
+// parent's sent row is added (two coalesced 256 B loads); the node's own fluid
+// row is then updated in place with its new exact maximum.  Rows with more than
+// PULL_LONG parents (the Zipf in-degree hubs) are left to k_ppr_pull_segs.
+__global__ void __launch_bounds__(PP_NT) k_ppr_pull(PprArgs a) {
+    __shared__ double s_red[PP_NT / 32];
+    const int lane = threadIdx.x & 31;
+    const int B = a.B;
+    const bool col0 = lane < B, col1 = lane + 32 < B;
+    const u64 active = a.ctl->active;
+    const bool own0 = col0 && ((active >> lane) & 1ull);
+    const bool own1 = col1 && ((active >> (lane + 32)) & 1ull);
+    double mx = 0.0;
+    const long long nw = (long long)gridDim.x * (PP_NT / 32);
+    for (long long i = blockIdx.x * (long long)(PP_NT / 32) + (threadIdx.x >> 5); i < a.n; i += nw) {
+        const u64 lo = a.in_off[i], hi = a.in_off[i + 1];
+        if (hi - lo > PULL_LONG) continue;
+        double acc0 = 0.0, acc1 = 0.0;
+        if (!pull_range(a, lo, hi, col0, col1, acc0, acc1)) continue;
+        mx = fmax(mx, pull_apply(a, i, col0, col1, own0, own1, acc0, acc1));
+    }
+    mx = block_max<PP_NT>(mx, s_red);
+    if (threadIdx.x == 0) a.part_max2[blockIdx.x] = mx;
+}
+
+// Hub rows, warp per segment of PULL_SEG parents: the partial row into seg_acc.
+__global__ void __launch_bounds__(PP_NT) k_ppr_pull_segs(PprArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int B = a.B;
+    const bool col0 = lane < B, col1 = lane + 32 < B;
+    const long long nw = (long long)gridDim.x * (PP_NT / 32);
+    for (long long q = blockIdx.x * (long long)(PP_NT / 32) + (threadIdx.x >> 5); q < a.nseg; q += nw) {
+        double acc0 = 0.0, acc1 = 0.0;
+        const u64 lo = a.seg_lo[q], hi = a.seg_hi[q];
+        pull_range(a, lo, hi, col0, col1, acc0, acc1);
+        double *P = a.seg_acc + (size_t)q * B;
+        if (col0) P[lane] = acc0;
+        if (col1) P[lane + 32] = acc1;
+    }
+}
+
+// Hub rows, warp per hub: its segments' partial rows added in segment order.
+__global__ void __launch_bounds__(PP_NT) k_ppr_pull_hubs(PprArgs a) {
+    __shared__ double s_red[PP_NT / 32];
+    const int lane = threadIdx.x & 31;
+    const int B = a.B;
+    const bool col0 = lane < B, col1 = lane + 32 < B;
+    const u64 active = a.ctl->active;
+    const bool own0 = col0 && ((active >> lane) & 1ull);
+    const bool own1 = col1 && ((active >> (lane + 32)) & 1ull);
+    double mx = 0.0;
+    const long long nw = (long long)gridDim.x * (PP_NT / 32);
+    for (long long h = blockIdx.x * (long long)(PP_NT / 32) + (threadIdx.x >> 5); h < a.nhub; h += nw) {
+        double acc0 = 0.0, acc1 = 0.0;
+        for (u32 q = a.hub_seg[h]; q < a.hub_seg[h + 1]; q++) {
+            const double *P = a.seg_acc + (size_t)q * B;
+            if (col0) acc0 += P[lane];
+            if (col1) acc1 += P[lane + 32];
+        }
+        mx = fmax(mx, pull_apply(a, a.hub_node[h], col0, col1, own0, own1, acc0, acc1));
+    }
+    mx = block_max<PP_NT>(mx, s_red);
+    if (threadIdx.x == 0) a.part_max2[a.nparts + blockIdx.x] = mx;
+}
+
 // Column masses |F_c|_1 (all columns, or only when a check is pending).
 __global__ void __launch_bounds__(PP_NT) k_ppr_mass(PprArgs a, int guarded) {
     __shared__ double s[PP_NT / 32][64];
@@ -173,10 +422,15 @@ __global__ void __launch_bounds__(PP_NT) k_ppr_mass(PprArgs a, int guarded) {
     double m0 = 0.0, m1 = 0.0, mx = 0.0;
     for (long long i = blockIdx.x * (long long)(PP_NT / 32) + wid; i < a.n; i += (long long)gridDim.x * (PP_NT / 32)) {
         const double *Fi = a.F + (size_t)i * B;
-        if (lane < B) m0 += fabs(Fi[lane]);
-        if (lane + 32 < B) m1 += fabs(Fi[lane + 32]);
-        if (lane < B) mx = fmax(mx, fabs(Fi[lane]));
-        if (lane + 32 < B) mx = fmax(mx, fabs(Fi[lane + 32]));
+        const double x0 = lane < B ? fabs(Fi[lane]) : 0.0;
+        const double x1 = lane + 32 < B ? fabs(Fi[lane + 32]) : 0.0;
+        m0 += x0;
+        m1 += x1;
+        mx = fmax(mx, fmax(x0, x1));
+        if (!guarded && a.rmax) {  // prologue of the pull formulation: exact row maxima
+            const double rm = warp_max_d(fmax(x0, x1));
+            if (lane == 0) a.rmax[i] = rm;
+        }
     }
     s[wid][lane] = m0;
     s[wid][lane + 32] = m1;
@@ -236,6 +490,7 @@ __global__ void k_ppr_finalize(PprArgs a) {
         u64 sel = 0, st = 0, pu = 0;
         for (int p = 0; p < a.nparts; p++) {
             mx = fmax(mx, a.part_max[p]);
+            if (a.in_off) mx = fmax(mx, fmax(a.part_max2[p], a.part_max2[a.nparts + p]));
             sel += a.part_sel[p];
             st += a.part_steps[p];
             pu += a.part_push[p];
@@ -320,6 +575,8 @@ struct fr_ppr {
     PprCtl *ctl;
     double *parts;
     u64 *parts64;
+    double *pull_buf;  // sent [n][B], rmax [n], part_max2 [2 grid], selection bitmap
+    void *hub_buf;     // hub rows of the pull: nodes, segment starts, segment ranges and partial rows
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     fr_solver_config cfg;
@@ -336,6 +593,46 @@ static int ppr_add(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *
     return FR_OK;
 }
 
+// prologue (theta0, masses, settle) then while { sweep (push, or take + pull),
+// finalize, mass?, check? }
+static int ppr_build_graph(fr_ppr *p) {
+    if (p->exec) { cudaGraphExecDestroy(p->exec); p->exec = nullptr; }
+    if (p->graph) { cudaGraphDestroy(p->graph); p->graph = nullptr; }
+    PprArgs &a = p->a;
+    FR_CUDA(cudaGraphCreate(&p->graph, 0));
+    FR_CUDA(cudaGraphConditionalHandleCreate(&a.cond, p->graph, 0, 0));
+    a.in_graph = 1;
+    static int zero = 0, one = 1;
+    void *args[] = {&a};
+    void *args0[] = {&a, &zero};
+    void *args1[] = {&a, &one};
+    cudaGraphNode_t n1, n2, nw;
+    FR_TRY(ppr_add(p->graph, &n1, nullptr, (void *)k_ppr_mass, p->grid, PP_NT, args0));
+    FR_TRY(ppr_add(p->graph, &n2, &n1, (void *)k_ppr_settle, 1, 64, args0));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = a.cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    FR_CUDA(cudaGraphAddNode(&nw, p->graph, &n2, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaGraphNode_t b0, bp, b1, b2, b3;
+    if (a.in_off) {
+        cudaGraphNode_t bs, bh;
+        FR_TRY(ppr_add(body, &b0, nullptr, (void *)k_ppr_take, p->grid, PP_NT, args));
+        FR_TRY(ppr_add(body, &bs, &b0, (void *)k_ppr_pull, p->grid, PP_NT, args));
+        FR_TRY(ppr_add(body, &bh, &bs, (void *)k_ppr_pull_segs, p->grid, PP_NT, args));
+        FR_TRY(ppr_add(body, &bp, &bh, (void *)k_ppr_pull_hubs, p->grid, PP_NT, args));
+    } else {
+        FR_TRY(ppr_add(body, &bp, nullptr, (void *)k_ppr_sweep, p->grid, PP_NT, args));
+    }
+    FR_TRY(ppr_add(body, &b1, &bp, (void *)k_ppr_finalize, 1, 64, args));
+    FR_TRY(ppr_add(body, &b2, &b1, (void *)k_ppr_mass, p->grid, PP_NT, args1));
+    FR_TRY(ppr_add(body, &b3, &b2, (void *)k_ppr_settle, 1, 64, args1));
+    FR_CUDA(cudaGraphInstantiate(&p->exec, p->graph, 0));
+    return FR_OK;
+}
+
 extern "C" int fr_ppr_destroy(fr_ppr *p) {
     if (!p) return FR_OK;
     if (p->exec) cudaGraphExecDestroy(p->exec);
@@ -343,6 +640,8 @@ extern "C" int fr_ppr_destroy(fr_ppr *p) {
     cudaFree(p->ctl);
     cudaFree(p->parts);
     cudaFree(p->parts64);
+    cudaFree(p->pull_buf);
+    cudaFree(p->hub_buf);
     delete p;
     return FR_OK;
 }
@@ -414,39 +713,7 @@ extern "C" int fr_ppr_create(int64_t n, int64_t m, const int64_t *d_offsets, con
         a.thr = cfg->target_error * (1.0 - cfg->damping);
         a.decay = cfg->decay;
         a.max_sweeps = cfg->max_sweeps > 0 ? cfg->max_sweeps : 1000000;
-        // graph: prologue (theta0, masses, settle) then while { sweep, finalize, mass?, check? }
-        if ((e = cudaGraphCreate(&p->graph, 0)) != cudaSuccess ||
-            (e = cudaGraphConditionalHandleCreate(&a.cond, p->graph, 0, 0)) != cudaSuccess) {
-            rc = cuda_fail(e, "graph", __FILE__, __LINE__);
-            break;
-        }
-        a.in_graph = 1;
-        static int zero = 0, one = 1;
-        void *args[] = {&a};
-        void *args0[] = {&a, &zero};
-        void *args1[] = {&a, &one};
-        cudaGraphNode_t n1, n2, nw;
-        if ((rc = ppr_add(p->graph, &n1, nullptr, (void *)k_ppr_mass, p->grid, PP_NT, args0)) != FR_OK) break;
-        if ((rc = ppr_add(p->graph, &n2, &n1, (void *)k_ppr_settle, 1, 64, args0)) != FR_OK) break;
-        cudaGraphNodeParams cp = {};
-        cp.type = cudaGraphNodeTypeConditional;
-        cp.conditional.handle = a.cond;
-        cp.conditional.type = cudaGraphCondTypeWhile;
-        cp.conditional.size = 1;
-        if ((e = cudaGraphAddNode(&nw, p->graph, &n2, 1, &cp)) != cudaSuccess) {
-            rc = cuda_fail(e, "while node", __FILE__, __LINE__);
-            break;
-        }
-        cudaGraph_t body = cp.conditional.phGraph_out[0];
-        cudaGraphNode_t b0, b1, b2, b3;
-        if ((rc = ppr_add(body, &b0, nullptr, (void *)k_ppr_sweep, p->grid, PP_NT, args)) != FR_OK) break;
-        if ((rc = ppr_add(body, &b1, &b0, (void *)k_ppr_finalize, 1, 64, args)) != FR_OK) break;
-        if ((rc = ppr_add(body, &b2, &b1, (void *)k_ppr_mass, p->grid, PP_NT, args1)) != FR_OK) break;
-        if ((rc = ppr_add(body, &b3, &b2, (void *)k_ppr_settle, 1, 64, args1)) != FR_OK) break;
-        if ((e = cudaGraphInstantiate(&p->exec, p->graph, 0)) != cudaSuccess) {
-            rc = cuda_fail(e, "instantiate", __FILE__, __LINE__);
-            break;
-        }
+        rc = ppr_build_graph(p);
     } while (0);
     if (rc != FR_OK) {
         fr_ppr_destroy(p);
@@ -454,6 +721,75 @@ extern "C" int fr_ppr_create(int64_t n, int64_t m, const int64_t *d_offsets, con
     }
     *out = p;
     return FR_OK;
+}
+
+// Switches a handle to the pull formulation over the transposed CSR (the
+// graph's in-edges: in_offsets int64[n+1], in_sources uint32[m], sources of
+// each row ascending, as graph.py to_matrix()).
+extern "C" int fr_ppr_set_pull(fr_ppr *p, const int64_t *d_in_offsets, const uint32_t *d_in_sources) {
+    if (!p || !d_in_offsets || (p->m > 0 && !d_in_sources)) {
+        set_error("fr_ppr_set_pull: need a handle and the transposed CSR");
+        return FR_ERR_ARG;
+    }
+    PprArgs &a = p->a;
+    if (!p->pull_buf) {
+        const size_t nb = (size_t)p->n * p->B + (size_t)p->n + 2 * (size_t)p->grid + ((size_t)p->n + 63) / 64 + 1;
+        cudaError_t e = cudaMalloc(&p->pull_buf, sizeof(double) * nb);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(ppr pull)", __FILE__, __LINE__);
+        a.sent = p->pull_buf;
+        a.rmax = a.sent + (size_t)p->n * p->B;
+        a.part_max2 = a.rmax + p->n;
+        a.selbits = reinterpret_cast<u32 *>(a.part_max2 + 2 * (size_t)p->grid);
+    }
+    // hub rows (more than PULL_LONG parents) and their PULL_SEG segments, from a
+    // host copy of the in-offsets (once per handle)
+    std::vector<int64_t> ioff((size_t)p->n + 1);
+    FR_CUDA(cudaMemcpy(ioff.data(), d_in_offsets, sizeof(int64_t) * ioff.size(), cudaMemcpyDeviceToHost));
+    std::vector<u32> hubs, hseg(1, 0);
+    std::vector<u64> slo;
+    for (long long i = 0; i < p->n; i++) {
+        const u64 lo = (u64)ioff[i], hi = (u64)ioff[i + 1];
+        if (hi - lo <= PULL_LONG) continue;
+        hubs.push_back((u32)i);
+        for (u64 b = lo; b < hi; b += PULL_SEG) slo.push_back(b);
+        hseg.push_back((u32)slo.size());
+    }
+    std::vector<u64> srange;  // segment ends
+    {
+        size_t q = 0;
+        for (size_t h = 0; h < hubs.size(); h++) {
+            const u64 hi = (u64)ioff[hubs[h] + 1];
+            for (; q < hseg[h + 1]; q++) srange.push_back(q + 1 < hseg[h + 1] ? slo[q + 1] : hi);
+        }
+    }
+    cudaFree(p->hub_buf);
+    p->hub_buf = nullptr;
+    const size_t nh = hubs.size(), ns = slo.size();
+    const size_t bytes = sizeof(u32) * (nh + nh + 1) + 16 + sizeof(u64) * 2 * ns + sizeof(double) * ns * p->B + 16;
+    cudaError_t e = cudaMalloc(&p->hub_buf, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(ppr hubs)", __FILE__, __LINE__);
+    char *b = (char *)p->hub_buf;
+    u64 *d_lo = (u64 *)b;
+    u64 *d_hi = d_lo + ns;
+    double *d_acc = (double *)(d_hi + ns);
+    u32 *d_hub = (u32 *)(d_acc + ns * p->B);
+    u32 *d_hseg = d_hub + nh;
+    if (ns) {
+        FR_CUDA(cudaMemcpy(d_lo, slo.data(), sizeof(u64) * ns, cudaMemcpyHostToDevice));
+        FR_CUDA(cudaMemcpy(d_hi, srange.data(), sizeof(u64) * ns, cudaMemcpyHostToDevice));
+    }
+    if (nh) FR_CUDA(cudaMemcpy(d_hub, hubs.data(), sizeof(u32) * nh, cudaMemcpyHostToDevice));
+    FR_CUDA(cudaMemcpy(d_hseg, hseg.data(), sizeof(u32) * (nh + 1), cudaMemcpyHostToDevice));
+    a.hub_node = d_hub;
+    a.hub_seg = d_hseg;
+    a.seg_lo = d_lo;
+    a.seg_hi = d_hi;
+    a.seg_acc = d_acc;
+    a.nhub = (u32)nh;
+    a.nseg = (u32)ns;
+    p->a.in_off = reinterpret_cast<const u64 *>(d_in_offsets);
+    p->a.in_src = d_in_sources;
+    return ppr_build_graph(p);
 }
 
 extern "C" int fr_ppr_run(fr_ppr *p, void *stream, fr_solve_stats *h_stats, double *h_col_residual) {

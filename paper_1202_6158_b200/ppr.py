@@ -27,7 +27,14 @@ def config4_seeds(n, B=64, k=10, seed=0):
 class BatchedPPR:
     """fr_ppr_* handle: graph + (n x B) state, reusable across solves."""
 
-    def __init__(self, graph, B, damping=0.85, target_error=1e-9, decay=0.6, max_sweeps=0):
+    MODES = ("push", "pull")
+
+    def __init__(self, graph, B, damping=0.85, target_error=1e-9, decay=0.6, max_sweeps=0, mode="push"):
+        """mode "push" (default, fastest): every edge visit scatters the row with
+        red.global.add; "pull": take + pull over the transposed CSR (no atomics,
+        bit-reproducible, Jacobi within a sweep: more sweeps)."""
+        if mode not in self.MODES:
+            raise ValueError(f"mode must be one of {sorted(self.MODES)}, got {mode!r}")
         if not 1 <= B <= 64:
             raise ValueError(f"B must be in [1, 64], got {B}")
         dev = require_device()
@@ -43,6 +50,10 @@ class BatchedPPR:
                                 ptr(self.fluid), ptr(self.history), ctypes.byref(cfg), stream_ptr(),
                                 ctypes.byref(handle)))
         self.handle = handle
+        self.mode = mode
+        if mode == "pull":
+            in_off, in_src = graph.reverse_csr()
+            check(lib.fr_ppr_set_pull(self.handle, ptr(in_off), ptr(in_src)))
 
     def solve(self, seeds):
         """seeds: (B, k) node ids.  Returns (rank n x B device tensor, stats, column residuals)."""
@@ -73,10 +84,10 @@ class BatchedPPR:
             pass
 
 
-def personalized_pagerank(graph, seeds, damping=0.85, target_error=1e-9, decay=0.6):
+def personalized_pagerank(graph, seeds, damping=0.85, target_error=1e-9, decay=0.6, mode="push"):
     """Rank vectors (n x B) for B seed sets (B x k), one batched device solve."""
     seeds = np.asarray(seeds)
-    p = BatchedPPR(graph, seeds.shape[0], damping, target_error, decay)
+    p = BatchedPPR(graph, seeds.shape[0], damping, target_error, decay, mode=mode)
     try:
         rank, stats, resid = p.solve(seeds)
     finally:

@@ -12,9 +12,18 @@ import torch  # noqa: E402
 import paper_1202_6158_b200 as fr  # noqa: E402
 from paper_1202_6158_b200 import gen  # noqa: E402
 
-g, _ = gen.baseline_graph(4)
+import argparse  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--local-frac", type=float, default=None, help="generator local fraction (diagnostic graphs)")
+ap.add_argument("--mode", default="push", help="push | pull | hybrid")
+args = ap.parse_args()
+if args.local_frac is None:
+    g, _ = gen.baseline_graph(4)
+else:
+    g, _ = gen.generate(gen.web_config(8.0, local_frac=args.local_frac), 1_000_000, 0, exact=True)
 seeds = fr.config4_seeds(g.n, 64, 10, seed=0)
-p = fr.BatchedPPR(g, 64, 0.85, 1e-9)
+p = fr.BatchedPPR(g, 64, 0.85, 1e-9, mode=args.mode)
 p.solve(seeds)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
