@@ -2,8 +2,12 @@
 nodes), random schedules (rule, theta policy, decay, beta, edge_frac), both
 fluid precisions, every kernel path with and without the single-block small
 graph solve, each rank checked against the oracle (the reference restated).
-Development tool (the test suite holds the fixed cases); prints one line per
-case and a summary, exits 1 on any failure."""
+Every 4th case also runs the power iteration against the oracle's (same
+iteration count, L1 <= 1e-12 plus 1e-9 * iterations of rounding), and every
+8th case (n >= 2) a batched personalized solve in both formulations (push,
+pull) against per-column oracle runs.  Development tool (the test suite holds
+the fixed cases); prints one line per case and a summary, exits 1 on any
+failure."""
 
 import os
 import random
@@ -53,7 +57,35 @@ for case in range(cases):
         ok = err <= bound and trace.rows[-1].residual <= target * (1 - damping) * (1 + 1e-9)
     except Exception as e:  # noqa: BLE001
         ok, err = False, repr(e)
+    extra = ""
+    if ok and case % 4 == 0 and damping < 1.0:
+        try:
+            x, _ = fr.power_iterate(g, fr.DiffusionParams(damping=damping, target_error=1e-10))
+            xr, it_r, _ = oracle.power_iterate(off, tgt, damping, 1e-10)
+            perr = float(np.abs(x - xr).sum())
+            ok = perr <= 1e-9
+            extra += f" power l1={perr:.2e} (oracle {it_r} it)"
+        except Exception as e:  # noqa: BLE001
+            ok, extra = False, extra + f" power {e!r}"
+    if ok and case % 8 == 0 and n >= 2:
+        B = rng.choice([1, 5, 64])
+        k = min(10, n)
+        seeds = fr.config4_seeds(n, B, k, seed=seed)
+        try:
+            worst = 0.0
+            for mode in ("push", "pull"):
+                r, _, res = fr.personalized_pagerank(g, seeds, damping=damping, target_error=1e-11, mode=mode)
+                r = r.cpu().numpy()
+                for c in range(min(B, 3)):
+                    v = np.zeros(n)
+                    np.add.at(v, seeds[c].astype(np.int64), 1.0 / k)
+                    ref = oracle.run_seq(off, tgt, damping, 1e-13, "sweep", teleport=v).rank
+                    worst = max(worst, float(np.abs(r[:, c] - ref).sum()))
+            ok = worst <= 2.5e-10 / (1 - damping)  # seeds may be dangling: |h|_1 < 1 scales the bound
+            extra += f" ppr(B={B}) push/pull l1<={worst:.2e}"
+        except Exception as e:  # noqa: BLE001
+            ok, extra = False, extra + f" ppr {e!r}"
     fails += not ok
-    print(f"{'ok  ' if ok else 'FAIL'} {desc}: l1={err}", flush=True)
+    print(f"{'ok  ' if ok else 'FAIL'} {desc}: l1={err}{extra}", flush=True)
 print(f"{cases - fails}/{cases} passed")
 sys.exit(1 if fails else 0)
