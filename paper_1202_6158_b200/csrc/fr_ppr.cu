@@ -20,6 +20,7 @@
 //     next take reads 8 B per row instead of the row.  The pull is Jacobi within
 //     a sweep (a push reaches its child in the next sweep).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -39,6 +40,8 @@ static constexpr int PP_SEGS = FR_PP_SEGS;
 static constexpr int PP_CHUNK = FR_PP_CHUNK;  // consecutive nodes per reservation (one warp per node)
 static constexpr u64 PULL_LONG = 1024;  // pull: rows with more parents are split into segments
 static constexpr u64 PULL_SEG = 2048;   // parents per segment
+static constexpr u32 PP_HOT_FLAG = 0x80000000u;
+static constexpr int PP_HOT_MAX = 32;   // hot rows per block: 32 x 64 fp64 = 16 KB of shared memory
 
 struct PprCtl {
     double theta;
@@ -70,6 +73,12 @@ struct PprArgs {
     const u32 *hub_node;  // [nhub]
     const u32 *hub_seg;   // [nhub + 1] first segment of each hub
     const u64 *seg_lo, *seg_hi;  // [nseg] in_src range of each segment
+    // push: the rows of the nhot highest in-degree nodes (Zipf hubs) are summed
+    // per block in shared memory and flushed once per block; tgt_enc is the
+    // column copy in which such targets carry PP_HOT_FLAG | slot
+    const u32 *tgt_enc;
+    const u32 *hot_node;  // [nhot]
+    int nhot;
     double *seg_acc;      // [nseg][B]
     u32 nhub, nseg;
     double *part_abs;    // [grid][64]
@@ -92,7 +101,8 @@ __device__ __forceinline__ double warp_max_d(double v) {
 }
 
 // Warp per node, nodes taken in order from PP_SEGS segments (as the scalar sweep).
-__global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
+__global__ void __launch_bounds__(PP_NT, 4) k_ppr_sweep(PprArgs a) {
+    extern __shared__ __align__(16) double hot_acc[];  // [nhot][B]
     __shared__ double s_abs[PP_NT / 32][64];
     __shared__ double s_red[PP_NT / 32];
     __shared__ u64 s_red64[PP_NT / 32];
@@ -106,6 +116,10 @@ __global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
     const bool own1 = lane + 32 < B && ((active >> (lane + 32)) & 1ull);
     double ab0 = 0.0, ab1 = 0.0, mx = 0.0;
     u64 nsel = 0, steps = 0, npush = 0;
+    const int nhot = a.nhot;
+    for (int q = threadIdx.x; q < nhot * B; q += PP_NT) hot_acc[q] = 0.0;
+    __syncthreads();
+    const u32 *__restrict__ tgt = nhot ? a.tgt_enc : a.tgt;
     const long long seg_len = (a.n + PP_SEGS - 1) / PP_SEGS;
     int seg = (int)((blockIdx.x * (PP_NT / 32) + wid) % PP_SEGS), misses = 0;
     long long node = 0, chunk_end = 0;
@@ -158,18 +172,33 @@ __global__ void __launch_bounds__(PP_NT) k_ppr_sweep(PprArgs a) {
                 npush += (u64)deg * ((own0 && p0 != 0.0) + (own1 && p1 != 0.0));
                 for (u32 k0 = 0; k0 < deg; k0 += 32) {
                     const u32 cnt = deg - k0 < 32u ? deg - k0 : 32u;
-                    const u32 tv = lane < cnt ? __ldg(a.tgt + lo + k0 + lane) : 0u;
-                    for (u32 j = 0; j < cnt; j++) {
+                    const u32 tv = lane < cnt ? __ldg(tgt + lo + k0 + lane) : 0u;
+                    // the encoded copy keeps each row's hot targets at its end, so the
+                    // batch's hot targets (if any) are lanes [cold, cnt)
+                    const u32 hm = nhot ? __ballot_sync(FULL, lane < cnt && (tv & PP_HOT_FLAG)) : 0u;
+                    const u32 cold = hm ? (u32)(__ffs(hm) - 1) : cnt;
+                    for (u32 j = 0; j < cold; j++) {
                         const u32 t = __shfl_sync(FULL, tv, j);
                         double *Ft = a.F + (size_t)t * B;
                         if (own0 && p0 != 0.0) red_add(Ft + lane, p0);
                         if (own1 && p1 != 0.0) red_add(Ft + lane + 32, p1);
+                    }
+                    for (u32 j = cold; j < cnt; j++) {  // one row of the block's table each
+                        const u32 t = __shfl_sync(FULL, tv, j);
+                        double *Ht = hot_acc + (size_t)(t & ~PP_HOT_FLAG) * B;
+                        if (own0 && p0 != 0.0) atomicAdd(Ht + lane, p0);
+                        if (own1 && p1 != 0.0) atomicAdd(Ht + lane + 32, p1);
                     }
                 }
             }
         }
         node++;
         have = node < chunk_end ? true : grab();
+    }
+    __syncthreads();  // every push into the hot table is done
+    for (int q = threadIdx.x; q < nhot * B; q += PP_NT) {
+        const double v = hot_acc[q];
+        if (v != 0.0) red_add(a.F + (size_t)a.hot_node[q / B] * B + q % B, v);
     }
     // per-column absorbed mass: lanes own columns, reduce over the block's warps
     s_abs[wid][lane] = ab0;
@@ -564,6 +593,44 @@ __global__ void k_ppr_scale(long long n, int B, const double *__restrict__ H, co
     }
 }
 
+// hot rows (push formulation): in-degree count and the encoded column copy
+__global__ void k_ppr_indeg(const u32 *__restrict__ tgt, long long m, u32 *__restrict__ cnt) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m; e += (long long)gridDim.x * blockDim.x)
+        atomicAdd(cnt + tgt[e], 1u);
+}
+// warp per row: the row's targets with the hot ones (PP_HOT_FLAG | slot) moved to
+// its end (order within a row does not matter to the pushes)
+__global__ void k_ppr_encode(const u64 *__restrict__ off, long long n, const u32 *__restrict__ tgt,
+                             const int *__restrict__ slot_of, u32 *__restrict__ enc) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        const u64 lo = off[i], hi = off[i + 1];
+        u32 nhot_row = 0;
+        for (u64 k0 = lo; k0 < hi; k0 += 32) {
+            const bool v = k0 + lane < hi;
+            const u32 t = v ? tgt[k0 + lane] : 0u;
+            nhot_row += __popc(__ballot_sync(0xffffffffu, v && slot_of[t] >= 0));
+        }
+        const u64 hot0 = hi - nhot_row;  // first position of the hot block
+        u32 seen_cold = 0, seen_hot = 0;
+        for (u64 k0 = lo; k0 < hi; k0 += 32) {
+            const bool v = k0 + lane < hi;
+            const u32 t = v ? tgt[k0 + lane] : 0u;
+            const int sl = v ? slot_of[t] : -1;
+            const u32 hm = __ballot_sync(0xffffffffu, v && sl >= 0);
+            const u32 cm = __ballot_sync(0xffffffffu, v && sl < 0);
+            const u32 below = (1u << lane) - 1u;
+            if (v) {
+                if (sl >= 0) enc[hot0 + seen_hot + __popc(hm & below)] = PP_HOT_FLAG | (u32)sl;
+                else enc[lo + seen_cold + __popc(cm & below)] = t;
+            }
+            seen_hot += __popc(hm);
+            seen_cold += __popc(cm);
+        }
+    }
+}
+
 }  // namespace fr
 
 using namespace fr;
@@ -577,14 +644,16 @@ struct fr_ppr {
     u64 *parts64;
     double *pull_buf;  // sent [n][B], rmax [n], part_max2 [2 grid], selection bitmap
     void *hub_buf;     // hub rows of the pull: nodes, segment starts, segment ranges and partial rows
+    u32 *hot_buf;      // push: encoded column copy [m] + hot row ids [nhot]
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     fr_solver_config cfg;
 };
 
 static int ppr_add(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *dep, void *func, int grid, int block,
-                   void **args) {
+                   void **args, unsigned smem = 0) {
     cudaKernelNodeParams p = {};
+    p.sharedMemBytes = smem;
     p.func = func;
     p.gridDim = dim3((unsigned)grid);
     p.blockDim = dim3((unsigned)block);
@@ -624,7 +693,8 @@ static int ppr_build_graph(fr_ppr *p) {
         FR_TRY(ppr_add(body, &bh, &bs, (void *)k_ppr_pull_segs, p->grid, PP_NT, args));
         FR_TRY(ppr_add(body, &bp, &bh, (void *)k_ppr_pull_hubs, p->grid, PP_NT, args));
     } else {
-        FR_TRY(ppr_add(body, &bp, nullptr, (void *)k_ppr_sweep, p->grid, PP_NT, args));
+        FR_TRY(ppr_add(body, &bp, nullptr, (void *)k_ppr_sweep, p->grid, PP_NT, args,
+                       (unsigned)(sizeof(double) * (size_t)a.nhot * (size_t)a.B)));
     }
     FR_TRY(ppr_add(body, &b1, &bp, (void *)k_ppr_finalize, 1, 64, args));
     FR_TRY(ppr_add(body, &b2, &b1, (void *)k_ppr_mass, p->grid, PP_NT, args1));
@@ -642,6 +712,7 @@ extern "C" int fr_ppr_destroy(fr_ppr *p) {
     cudaFree(p->parts64);
     cudaFree(p->pull_buf);
     cudaFree(p->hub_buf);
+    cudaFree(p->hot_buf);
     delete p;
     return FR_OK;
 }
@@ -713,6 +784,45 @@ extern "C" int fr_ppr_create(int64_t n, int64_t m, const int64_t *d_offsets, con
         a.thr = cfg->target_error * (1.0 - cfg->damping);
         a.decay = cfg->decay;
         a.max_sweeps = cfg->max_sweeps > 0 ? cfg->max_sweeps : 1000000;
+        // hot rows: the nhot highest in-degree nodes (FR_PP_HOT, default 16; 0 = off)
+        a.nhot = 0;
+        {
+            const char *env = getenv("FR_PP_HOT");
+            int want = env ? atoi(env) : 16;
+            want = std::max(0, std::min(want, PP_HOT_MAX));
+            if (want > n) want = (int)n;
+            if (want > 0 && m > 0 && n < (1ll << 31)) {
+                Scratch scratch((cudaStream_t)stream);
+                u32 *cnt;
+                int *slot_of;
+                if ((rc = scratch.alloc(&cnt, (size_t)n)) != FR_OK) break;
+                if ((rc = scratch.alloc(&slot_of, (size_t)n)) != FR_OK) break;
+                cudaStream_t st = (cudaStream_t)stream;
+                cudaMemsetAsync(cnt, 0, sizeof(u32) * (size_t)n, st);
+                k_ppr_indeg<<<di.sms * 8, 256, 0, st>>>(d_targets, m, cnt);
+                std::vector<u32> hc((size_t)n);
+                cudaMemcpyAsync(hc.data(), cnt, sizeof(u32) * (size_t)n, cudaMemcpyDeviceToHost, st);
+                if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "ppr in-degree", __FILE__, __LINE__); break; }
+                std::vector<u32> idx((size_t)n);
+                for (long long i = 0; i < n; i++) idx[i] = (u32)i;
+                std::partial_sort(idx.begin(), idx.begin() + want, idx.end(),
+                                  [&](u32 x, u32 y) { return hc[x] != hc[y] ? hc[x] > hc[y] : x < y; });
+                std::vector<int> so((size_t)n, -1);
+                for (int k = 0; k < want; k++) so[idx[k]] = k;
+                if ((e = cudaMalloc(&p->hot_buf, sizeof(u32) * ((size_t)m + want))) != cudaSuccess) {
+                    rc = cuda_fail(e, "cudaMalloc(ppr hot rows)", __FILE__, __LINE__);
+                    break;
+                }
+                cudaMemcpyAsync(slot_of, so.data(), sizeof(int) * (size_t)n, cudaMemcpyHostToDevice, st);
+                k_ppr_encode<<<di.sms * 8, 256, 0, st>>>(reinterpret_cast<const u64 *>(d_offsets), n, d_targets,
+                                                         slot_of, p->hot_buf);
+                cudaMemcpyAsync(p->hot_buf + m, idx.data(), sizeof(u32) * want, cudaMemcpyHostToDevice, st);
+                if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e, "ppr encode", __FILE__, __LINE__); break; }
+                a.tgt_enc = p->hot_buf;
+                a.hot_node = p->hot_buf + m;
+                a.nhot = want;
+            }
+        }
         rc = ppr_build_graph(p);
     } while (0);
     if (rc != FR_OK) {

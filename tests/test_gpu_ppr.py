@@ -126,3 +126,25 @@ def test_batched_ppr_pull_hub_rows(cuda, oracle):
     a, b = a.cpu().numpy(), b.cpu().numpy()
     for c in range(4):
         assert np.abs(a[:, c] - b[:, c]).sum() <= 2e-9, c
+
+
+@pytest.mark.parametrize("hot", ["0", "1", "32"])
+def test_batched_ppr_hot_rows(cuda, oracle, monkeypatch, hot):
+    """The push formulation sums the pushes into the highest in-degree rows in a
+    per-block shared-memory table (FR_PP_HOT rows, default 16); with 0, 1 or 32 such
+    rows every column matches the reference run with its teleport vector."""
+    from paper_1202_6158_b200 import ppr
+    monkeypatch.setenv("FR_PP_HOT", hot)
+    n, B = 5000, 6
+    src, dst = oracle.gen_edges(oracle.web_config(8.0), n, 21)
+    off, tgt, _ = oracle.csr_build(n, src, dst, clean=True)
+    g = cuda.SparseGraph(n, off, tgt.astype(np.int32))
+    seeds = ppr.config4_seeds(n, B, 10, seed=8)
+    rank, _, resid = ppr.personalized_pagerank(g, seeds, target_error=1e-11)
+    assert max(resid) <= 1e-11 * 0.15
+    rank = rank.cpu().numpy()
+    for c in range(B):
+        v = np.zeros(n)
+        np.add.at(v, seeds[c].astype(np.int64), 1.0 / 10)
+        ref = oracle.run_seq(off, tgt, 0.85, 1e-13, "sweep", teleport=v).rank
+        assert np.abs(rank[:, c] - ref).sum() <= 1e-9, c
