@@ -78,7 +78,6 @@ struct SolveCtl {
     u64 next_trace;     // sampled runs: record the true error once diffusions reach this
     // everything above is the header copied back after a run
     u64 seg_next[SW_MAX_SEGS * SEG_PAD];  // fused path: in-order tile counters, one 128 B line each
-    u32 ticket[2];  // last-block tickets of the merged graph kernels (fold + finalize, mass + check)
 };
 
 enum { PATH_FUSED = 0, PATH_BINNED = 1, PATH_OWNED = 2 };
@@ -152,35 +151,12 @@ static constexpr u32 HOT_FLAG = 0x80000000u;
 #define FR_BLK_COLD 1
 #endif
 
-// Whether this block is the last of its grid to get here (the others' global
-// writes before the call are then visible to it); the ticket is re-armed.
-__device__ __forceinline__ bool last_block(u32 *ticket) {
-    __shared__ u32 s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const u32 t = atomicAdd(ticket, 1u);
-        s_last = t == gridDim.x - 1 ? 1u : 0u;
-        if (s_last) *ticket = 0u;
-    }
-    __syncthreads();
-    if (!s_last) return false;
-    __threadfence();
-    return true;
-}
-
 // ------------------------------------------------------------------ prologue
 // Exact sum |F| and max score.  guarded: only when the fused path asked for a check.
 template <typename FT>
-__device__ void k_mass_partials_body(const SweepArgs<FT> &a);
-template <typename FT>
 __global__ void __launch_bounds__(SEL_NT) k_mass_partials(SweepArgs<FT> a, int guarded) {
-    if (guarded && !a.ctl->need_check) return;
-    k_mass_partials_body(a);
-}
-template <typename FT>
-__device__ void k_mass_partials_body(const SweepArgs<FT> &a) {
     __shared__ double sm[SEL_NT / 32];
+    if (guarded && !a.ctl->need_check) return;
     double mass = 0.0, mx = 0.0, neg = 0.0;
     for (long long i = blockIdx.x * (long long)SEL_NT + threadIdx.x; i < a.n; i += (long long)gridDim.x * SEL_NT) {
         const double f = (double)a.F[i];
@@ -199,16 +175,6 @@ __device__ void k_mass_partials_body(const SweepArgs<FT> &a) {
         a.part_max[blockIdx.x] = bx;
         a.part_abs[blockIdx.x] = bn;  // most negative fluid (the prologue's signed test)
     }
-}
-
-template <typename FT>
-__device__ void mass_check_block(const SweepArgs<FT> &a, int nparts);
-// Graph path: the guarded exact mass and (last block) its check in one node.
-template <typename FT>
-__global__ void __launch_bounds__(SEL_NT) k_mass_partials_check(SweepArgs<FT> a, int nparts) {
-    if (!a.ctl->need_check) return;  // uniform over the grid: no block takes a ticket
-    k_mass_partials_body(a);
-    if (last_block(&a.ctl->ticket[1])) mass_check_block(a, nparts);
 }
 
 template <typename FT>
@@ -241,16 +207,10 @@ __global__ void __launch_bounds__(FIN_NT) k_prologue(SweepArgs<FT> a, int nparts
 // Fused path: exact check of the stopping rule once the incremental residual
 // says we are done (engine.py:290-293 re-derives the residual the same way).
 template <typename FT>
-__device__ void mass_check_block(const SweepArgs<FT> &a, int nparts);
-template <typename FT>
 __global__ void __launch_bounds__(FIN_NT) k_mass_check(SweepArgs<FT> a, int nparts) {
-    if (!a.ctl->need_check) return;
-    mass_check_block(a, nparts);
-}
-template <typename FT>
-__device__ void mass_check_block(const SweepArgs<FT> &a, int nparts) {
     __shared__ double sm[FIN_NT / 32];
     SolveCtl *c = a.ctl;
+    if (!c->need_check) return;
     double mass = 0.0;
     for (int p = threadIdx.x; p < nparts; p += FIN_NT) mass += a.part_mass[p];
     mass = block_sum<FIN_NT>(mass, sm);
@@ -1115,28 +1075,7 @@ __device__ bool finalize_sweep(const SweepArgs<FT> &a, double mass, double ab, d
                                u64 hsteps);
 
 template <typename FT>
-__device__ void finalize_block(const SweepArgs<FT> &a, int nparts);
-template <typename FT>
 __global__ void __launch_bounds__(FIN_NT) k_finalize(SweepArgs<FT> a, int nparts) {
-    finalize_block(a, nparts);
-}
-
-// Graph path: the fold of the warm slots, then (last block) the sweep's bookkeeping
-// -- one kernel node instead of k_fold + k_finalize.
-template <typename FT>
-__global__ void __launch_bounds__(256) k_fold_finalize(SweepArgs<FT> a, int nparts) {
-    for (u32 s = blockIdx.x * blockDim.x + threadIdx.x; s < a.nslots; s += gridDim.x * blockDim.x) {
-        const FT v = a.Fw[s];
-        if (v != (FT)0) {
-            a.F[a.slot_node[s]] += v;
-            a.Fw[s] = (FT)0;
-        }
-    }
-    if (last_block(&a.ctl->ticket[0])) finalize_block(a, nparts);
-}
-
-template <typename FT>
-__device__ void finalize_block(const SweepArgs<FT> &a, int nparts) {
     __shared__ double sm[FIN_NT / 32];
     __shared__ u64 sm64[FIN_NT / 32];
     double mass = 0.0, ab = 0.0, mx = 0.0;
@@ -1558,15 +1497,14 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     if (fused_like(a.path)) {
         // sweep -> hub pushes -> finalize -> (guarded) exact mass -> (guarded) check
-        // (fold + finalize and mass + check are one node each: the last block of the
-        // first part runs the second; ticket counters in SolveCtl)
-        cudaGraphNode_t n_sw, n_hub, n_fin, n_chk;
+        cudaGraphNode_t n_sw, n_hub, n_fold, n_fin, n_m, n_chk;
         FR_TRY(add_kernel<FT>(body, &n_sw, nullptr, 0, sweep_kernel(a), s->sweep_grid, sweep_threads(a), args_a,
                               sweep_smem(a)));
         FR_TRY(add_kernel<FT>(body, &n_hub, &n_sw, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
-        FR_TRY(add_kernel<FT>(body, &n_fin, &n_hub, 1, (void *)k_fold_finalize<FT>, s->fold_grid, 256, args_ans));
-        FR_TRY(add_kernel<FT>(body, &n_chk, &n_fin, 1, (void *)k_mass_partials_check<FT>, s->sel_grid, SEL_NT,
-                              args_an));
+        FR_TRY(add_kernel<FT>(body, &n_fold, &n_hub, 1, (void *)k_fold<FT>, s->fold_grid, 256, args_a));
+        FR_TRY(add_kernel<FT>(body, &n_fin, &n_fold, 1, (void *)k_finalize<FT>, 1, FIN_NT, args_ans));
+        FR_TRY(add_kernel<FT>(body, &n_m, &n_fin, 1, (void *)k_mass_partials<FT>, s->sel_grid, SEL_NT, args_m1));
+        FR_TRY(add_kernel<FT>(body, &n_chk, &n_m, 1, (void *)k_mass_check<FT>, 1, FIN_NT, args_an));
     } else {
         // select -> three push bins (concurrent) -> fold of the warm slots -> finalize
         cudaGraphNode_t n_sel, n_p[3], n_fold, n_fin;
