@@ -78,6 +78,10 @@ struct SolveCtl {
     u64 next_trace;     // sampled runs: record the true error once diffusions reach this
     // everything above is the header copied back after a run
     u64 seg_next[SW_MAX_SEGS * SEG_PAD];  // fused path: in-order tile counters, one 128 B line each
+    // owned path in a graph (hub_defer): hub rows queued in sweep s (queue s & 1) are
+    // pushed by the blocks of sweep s + 1 between their chunks, the last sweep's by a
+    // drain after the loop
+    u32 hub_cnt[2], hub_next[2];
 };
 
 enum { PATH_FUSED = 0, PATH_BINNED = 1, PATH_OWNED = 2 };
@@ -117,6 +121,8 @@ struct SweepArgs {
     u32 chunk;   // fused path: tiles per reservation
     u32 own_ch;  // owned path: nodes per block-owned chunk (power of two)
     u32 own_rev;  // owned path: odd sweeps run in descending node order
+    int hub_defer;  // owned path in a graph: hub rows pushed one sweep later by the sweep kernel (SolveCtl::hub_cnt)
+    u32 hub_stride;  // entries per parity of the deferred hub queue (qnode[2] / qval[2])
 
     // sampled runs (fr_solver_run_sampled, single-block path): true L1 error of the
     // normalized history against ref every trace_every diffusions, into true_err[row]
@@ -158,6 +164,15 @@ __global__ void __launch_bounds__(SEL_NT) k_mass_partials(SweepArgs<FT> a, int g
     __shared__ double sm[SEL_NT / 32];
     if (guarded && !a.ctl->need_check) return;
     double mass = 0.0, mx = 0.0, neg = 0.0;
+    if (a.hub_defer) {
+        // hub rows taken by the last sweep and not pushed yet: d*f each, |q| * deg
+        const u32 par = (u32)((a.ctl->sweeps + 1) & 1);
+        const u32 cnt = a.ctl->hub_cnt[par];
+        for (u32 q = blockIdx.x * SEL_NT + threadIdx.x; q < cnt; q += gridDim.x * SEL_NT) {
+            const u32 node = a.qnode[2][par * a.hub_stride + q];
+            mass += fabs((double)a.qval[2][par * a.hub_stride + q]) * (double)(a.off[node + 1] - a.off[node]);
+        }
+    }
     for (long long i = blockIdx.x * (long long)SEL_NT + threadIdx.x; i < a.n; i += (long long)gridDim.x * SEL_NT) {
         const double f = (double)a.F[i];
         const double af = fabs(f);
@@ -610,6 +625,39 @@ __device__ __forceinline__ double take_shared(double *p) {
 }
 __device__ __forceinline__ float take_shared(float *p) { return atomicExch(p, 0.0f); }
 
+// Deferred hub rows (hub_defer): the whole block claims one row queued by the
+// previous sweep and pushes it (128 threads over its columns, as k_push_block;
+// hot targets into the block's table).  Returns false when none is left.
+template <typename FT>
+__device__ bool own_hub_row(const SweepArgs<FT> &a, FT *hot_acc, u64 sweep) {
+    __shared__ u32 hub_sm;
+    const u32 par = (u32)((sweep + 1) & 1);  // the queue of sweep - 1
+    SolveCtl *c = a.ctl;
+    if (threadIdx.x == 0) {
+        const u32 cnt = c->hub_cnt[par];
+        u32 k = ~0u;
+        if (c->hub_next[par] < cnt) {
+            k = atomicAdd(&c->hub_next[par], 1u);
+            if (k >= cnt) k = ~0u;
+        }
+        hub_sm = k;
+    }
+    __syncthreads();
+    const u32 k = hub_sm;
+    __syncthreads();  // hub_sm is read by every thread before the next call writes it
+    if (k == ~0u) return false;
+    const u32 q = k + par * a.hub_stride;
+    const u32 node = a.qnode[2][q];
+    const FT v = a.qval[2][q];
+    const u64 lo = a.off[node], hi = a.off[node + 1];
+    const u64 pol = FR_BLK_COLD ? policy_evict_first() : 0ull;
+    const bool slotted = a.nslots != 0;
+#pragma unroll 4
+    for (u64 e = lo + threadIdx.x; e < hi; e += OWN_NT)
+        push_far(a.F, a.Fw, hot_acc, a.nhot, __ldg(a.tgt + e), v, slotted, node, pol);
+    return true;
+}
+
 template <typename FT, bool WIDE>
 __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(SweepArgs<FT> a) {
     using OT = typename std::conditional<WIDE, u64, u32>::type;
@@ -799,10 +847,12 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
             if (hmask) {
                 u32 hb = 0;
                 const int leader = __ffs(hmask) - 1;
-                if (lane == leader) hb = atomicAdd(&a.ctl->qcount[2], (u32)__popc(hmask));
+                if (lane == leader) hb = atomicAdd(a.hub_defer ? &a.ctl->hub_cnt[sweep & 1] : &a.ctl->qcount[2],
+                                                   (u32)__popc(hmask));
                 hb = __shfl_sync(FULL, hb, leader);
                 if (hub) {
-                    const u32 q = hb + __popc(hmask & ((1u << lane) - 1u));
+                    const u32 q = hb + __popc(hmask & ((1u << lane) - 1u)) +
+                                  (a.hub_defer ? (u32)(sweep & 1) * a.hub_stride : 0u);
                     a.qnode[2][q] = (u32)i;
                     a.qval[2][q] = pvf;
                     hsteps += deg;
@@ -851,7 +901,11 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                 acc[q] = (FT)0;
             }
         }
+        if (a.hub_defer) own_hub_row(a, hot_acc, sweep);  // one hub row of the previous sweep per chunk
     }
+    if (a.hub_defer)
+        while (own_hub_row(a, hot_acc, sweep)) {
+        }
     hot_flush(a.Fw, hot_acc, a.nhot, OWN_NT);
     const double ba = block_sum<OWN_NT>(absorbed, red_sm);
     const double bx = block_max<OWN_NT>(mx, red_sm);
@@ -1016,7 +1070,10 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
     __shared__ __align__(128) u32 stage[BLK_STAGES][BLK_CHUNK];
     __shared__ __align__(8) u64 bar[BLK_STAGES];
     __shared__ FT hot_acc[HOT_SLOTS];
-    const u32 cnt = a.ctl->qcount[2];
+    // hub_defer: the drain after the loop, over the rows the last sweep queued
+    const u32 par = (u32)((a.ctl->sweeps + 1) & 1);
+    const u32 cnt = a.hub_defer ? a.ctl->hub_cnt[par] : a.ctl->qcount[2];
+    const u32 qoff = a.hub_defer ? par * a.hub_stride : 0u;
     if (blockIdx.x >= cnt) return;
     const u64 pol = FR_BLK_COLD ? policy_evict_first() : 0ull;
     if (threadIdx.x == 0) {
@@ -1027,8 +1084,8 @@ __global__ void __launch_bounds__(BLK_NT) k_push_block(SweepArgs<FT> a) {
     __syncthreads();
     u32 seq = 0;  // chunks consumed by this block so far (slot = seq % STAGES, parity = (seq / STAGES) & 1)
     for (u32 e = blockIdx.x; e < cnt; e += gridDim.x) {
-        const u32 node = a.qnode[2][e];
-        const FT v = a.qval[2][e];
+        const u32 node = a.qnode[2][qoff + e];
+        const FT v = a.qval[2][qoff + e];
         const u64 lo = a.off[node], hi = a.off[node + 1];
         const u64 a0 = min(hi, (lo + 3) & ~3ull);
         const u64 a1 = max(a0, hi & ~3ull);
@@ -1151,6 +1208,10 @@ __device__ bool finalize_sweep(const SweepArgs<FT> &a, double mass, double ab, d
         while (th > mx) th *= a.decay;
     c->theta = th;
     c->qcount[0] = c->qcount[1] = c->qcount[2] = 0;
+    // deferred hub rows: the queue the sweep just consumed (its blocks exited only
+    // once it was empty) is free for the next sweep's rows
+    c->hub_cnt[c->sweeps & 1] = 0;
+    c->hub_next[c->sweeps & 1] = 0;
     for (int q = 0; q < SW_MAX_SEGS; q++) c->seg_next[q * SEG_PAD] = 0;
     const bool budget = (long long)c->sweeps >= a.max_sweeps ||
                         (a.max_diffusions > 0 && (long long)c->diffusions >= a.max_diffusions);
@@ -1476,6 +1537,8 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
     FR_CUDA(cudaGraphCreate(&s->graph, 0));
     FR_CUDA(cudaGraphConditionalHandleCreate(&a.cond, s->graph, 0, 0));
     a.in_graph = 1;
+    const char *ed = getenv("FR_HUB_DEFER");
+    a.hub_defer = a.path == PATH_OWNED && a.hub_stride != 0 && (ed ? atoi(ed) != 0 : true) ? 1 : 0;
     int nparts = s->sel_grid;
     int nparts_sw = s->sweep_grid;
     int unguarded = 0, guarded = 1;
@@ -1497,10 +1560,17 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     if (fused_like(a.path)) {
         // sweep -> hub pushes -> finalize -> (guarded) exact mass -> (guarded) check
+        // owned path: the hub rows queued by a sweep are pushed by the next sweep's
+        // blocks between their chunks (no hub node in the loop), the last sweep's by a
+        // drain after the loop
         cudaGraphNode_t n_sw, n_hub, n_fold, n_fin, n_m, n_chk;
         FR_TRY(add_kernel<FT>(body, &n_sw, nullptr, 0, sweep_kernel(a), s->sweep_grid, sweep_threads(a), args_a,
                               sweep_smem(a)));
-        FR_TRY(add_kernel<FT>(body, &n_hub, &n_sw, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
+        if (a.hub_defer) {
+            n_hub = n_sw;
+        } else {
+            FR_TRY(add_kernel<FT>(body, &n_hub, &n_sw, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
+        }
         FR_TRY(add_kernel<FT>(body, &n_fold, &n_hub, 1, (void *)k_fold<FT>, s->fold_grid, 256, args_a));
         FR_TRY(add_kernel<FT>(body, &n_fin, &n_fold, 1, (void *)k_finalize<FT>, 1, FIN_NT, args_ans));
         FR_TRY(add_kernel<FT>(body, &n_m, &n_fin, 1, (void *)k_mass_partials<FT>, s->sel_grid, SEL_NT, args_m1));
@@ -1514,6 +1584,12 @@ static int build_graph(fr_solver *s, SweepArgs<FT> &a) {
         FR_TRY(add_kernel<FT>(body, &n_p[2], &n_sel, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT, args_a));
         FR_TRY(add_kernel<FT>(body, &n_fold, n_p, 3, (void *)k_fold<FT>, s->fold_grid, 256, args_a));
         FR_TRY(add_kernel<FT>(body, &n_fin, &n_fold, 1, (void *)k_finalize<FT>, 1, FIN_NT, args_an));
+    }
+    if (a.hub_defer) {  // the rows the last sweep queued, then the warm slots they filled
+        cudaGraphNode_t n_drain, n_dfold;
+        FR_TRY(add_kernel<FT>(s->graph, &n_drain, &n_while, 1, (void *)k_push_block<FT>, s->block_grid, BLK_NT,
+                              args_a));
+        FR_TRY(add_kernel<FT>(s->graph, &n_dfold, &n_drain, 1, (void *)k_fold<FT>, s->fold_grid, 256, args_a));
     }
     FR_CUDA(cudaGraphInstantiate(&s->exec, s->graph, 0));
     return FR_OK;
@@ -1706,8 +1782,11 @@ static int setup(fr_solver *s, SweepArgs<FT> &a, const int64_t *d_offsets, const
     const long long cap0 = binned ? n : 0;
     const long long cap1 = binned ? std::min<long long>(n, m / ((long long)a.t0 + 1) + 1) : 0;
     const long long cap2 = std::min<long long>(n, m / (long long)a.t2 + 1);
-    FR_TRY(pool_alloc(&s->qnode_buf, sizeof(u32) * (size_t)(cap0 + cap1 + cap2 + 3), st));
-    FR_TRY(pool_alloc(&s->qval_buf, sizeof(FT) * (size_t)(cap0 + cap1 + cap2 + 3), st));
+    // the owned path's deferred hub rows use two queues (sweep parity) of cap2 + 1
+    const long long cap2x = c.kernel_path == 2 ? 2 * (cap2 + 1) : cap2;
+    a.hub_stride = c.kernel_path == 2 && cap2 + 1 < (1ll << 31) ? (u32)(cap2 + 1) : 0u;
+    FR_TRY(pool_alloc(&s->qnode_buf, sizeof(u32) * (size_t)(cap0 + cap1 + cap2x + 3), st));
+    FR_TRY(pool_alloc(&s->qval_buf, sizeof(FT) * (size_t)(cap0 + cap1 + cap2x + 3), st));
     u32 *qn = (u32 *)s->qnode_buf;
     FT *qv = (FT *)s->qval_buf;
     a.qnode[0] = qn;
@@ -1916,6 +1995,7 @@ template <typename FT>
 static int run_profiled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, fr_solve_stats *h_stats, double *ms,
                         int64_t *launches) {
     a.in_graph = 0;
+    a.hub_defer = 0;  // host-launched sweeps push the hub rows after each sweep (k_push_block)
     int nparts = s->sel_grid, nparts_sw = s->sweep_grid;
     FR_TRY(reset_ctl(s, st));
     if (s->small) {  // one launch: all of it is class 0
@@ -2008,6 +2088,7 @@ template <typename FT>
 static int run_sampled(fr_solver *s, SweepArgs<FT> a, cudaStream_t st, const double *ref, long long every,
                        fr_solve_stats *h_stats) {
     FR_TRY(reset_ctl(s, st));
+    a.hub_defer = 0;
     a.ref = ref;
     a.trace_every = every;
     a.true_err = s->true_err;

@@ -496,3 +496,41 @@ def test_signed_fluid_residual_refresh(cuda, oracle, monkeypatch, path, small):
     off, tgt, _ = oracle.csr_build(n, src.astype(np.uint32), dst.astype(np.uint32), clean=False)
     ref = oracle.run_seq(off, tgt, 0.85, 1e-13, "sweep", fluid=f0)
     assert l1(state.history, ref.history) <= 2e-10
+
+
+@pytest.mark.parametrize("defer", ["1", "0"])
+def test_owned_deferred_hub_rows(cuda, oracle, monkeypatch, defer):
+    """Rows with >= 2048 children: in the CUDA-graph loop of the owned path they are queued by
+    one sweep and pushed by the next sweep's blocks (FR_HUB_DEFER, default on), the last
+    sweep's by a drain after the loop.  Exact conservation after a budget stop (nothing left
+    in flight) and the rank of a full solve against the oracle."""
+    monkeypatch.setenv("FR_HUB_DEFER", defer)
+    monkeypatch.setenv("FR_SMALL", "0")
+    n = 150_000
+    src, dst = oracle.gen_edges(oracle.web_config(8.0), n, 47)
+    rng = np.random.default_rng(3)
+    hubs = [17, 40_000, 90_001, 149_990]
+    src = np.concatenate([src] + [np.full(3000, h, dtype=np.uint32) for h in hubs])
+    dst = np.concatenate([dst] + [rng.choice(n, 3000, replace=False).astype(np.uint32) for _ in hubs])
+    off, tgt, _ = oracle.csr_build(n, src, dst, clean=True)
+    assert (np.diff(off)[hubs] >= 2048).all()
+    g = graph_from(cuda, off, tgt)
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.6, degree_exponent=0.85,
+                                edge_frac=0.2, kernel_path="owned")
+    params = cuda.DiffusionParams(target_error=1e-12)
+    state = cuda.init(g, params)
+    f0 = state.fluid.cpu().numpy().copy()
+    cuda.run(g, params, sched, state=state, max_sweeps=6)
+    torch.cuda.synchronize()
+    h = state.history.cpu().numpy()
+    f = state.fluid.cpu().numpy()
+    deg = np.diff(off)
+    src_e = np.repeat(np.arange(g.n), deg)
+    push = np.zeros(g.n)
+    np.add.at(push, tgt.astype(np.int64), h[src_e] / deg[src_e])
+    assert np.abs(h + f - f0 - 0.85 * push).max() <= 1e-15
+    assert state.sweeps == 6
+    params = cuda.DiffusionParams(target_error=1e-10)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-12, "sweep").rank
+    rank, _ = cuda.run(g, params, sched)
+    assert l1(rank, ref) <= 1e-9
