@@ -12,7 +12,11 @@
 //                  into the block's own chunk are summed in shared memory and
 //                  taken by the chunk's later tiles in the same sweep
 //                  (Gauss-Seidel), the rest flushed to F at the chunk end; odd
-//                  sweeps run backwards; then k_push_block, k_fold, k_finalize
+//                  sweeps run backwards; rows with >= t2 children are queued and,
+//                  in the CUDA-graph loop, pushed by the next sweep's blocks
+//                  between their chunks (the last sweep's by a k_push_block drain
+//                  after the loop; host-launched sweeps run k_push_block after
+//                  each sweep); then k_fold, k_finalize
 //
 // Fused path (kernel_path = 0), one sweep:
 //   k_sweep        warp per tile of 32 consecutive nodes, tiles taken in order
