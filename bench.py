@@ -310,10 +310,15 @@ def run_ours(args, world, rank, local):
     ms_per_step = ms_max / args.steps
     last = stats[-1]
     rows = solver.trace_rows()
-    # our kernels in the timed region: init (1) + graph prologue (2) + per sweep (fused: sweep, hub,
-    # fold, finalize, guarded mass pass, guarded check = 6; binned: 5) + exact residual (2) + normalize (3)
-    per_sweep = 5 if args.path == "binned" else 6
-    launches = sum(1 + 2 + per_sweep * s + 2 + 3 for s in sweeps)
+    # our kernels in the timed region: init (1) + graph prologue (2) + per sweep (owned: sweep, fold,
+    # finalize, guarded mass pass, guarded check = 5, its hub rows pushed inside the next sweep;
+    # fused: + hub = 6; binned: 5) + owned: hub drain and fold after the loop (2) + exact residual (2)
+    # + normalize (3)
+    per_sweep = 6 if args.path == "fused" else 5
+    after_loop = 2 if args.path == "owned" and os.environ.get("FR_HUB_DEFER", "1") != "0" else 0
+    if args.path == "owned" and not after_loop:
+        per_sweep = 6
+    launches = sum(1 + 2 + per_sweep * s + after_loop + 2 + 3 for s in sweeps)
 
     # correctness guard for the measured run: stopping rule met, rank normalized
     assert last.residual <= params.target_error * (1 - params.damping) * 1.0000001, last.residual
