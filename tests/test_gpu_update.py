@@ -86,3 +86,36 @@ def test_resume_matches_fresh_run(cuda):
         resumed, _ = update.resume(state, g2, params, cuda.make_scheduler("sweep"))
         fresh, _ = cuda.run(g2, params, cuda.make_scheduler("sweep"))
         assert float(np.abs(resumed - fresh).sum()) <= 2 * params.target_error
+
+
+def test_resume_with_hub_rows_on_the_owned_graph_path(cuda, oracle, monkeypatch):
+    """Signed fluid through the CUDA-graph owned path of a large graph whose rows with >= 2048
+    children are pushed one sweep late (deferred hub rows, their in-flight fluid counted in the
+    exact residual checks): the resumed rank matches a fresh solve of the edited graph."""
+    from paper_1202_6158_b200 import update
+    monkeypatch.setenv("FR_SMALL", "0")
+    n = 150_000
+    src, dst = oracle.gen_edges(oracle.web_config(8.0), n, 5)
+    rng = np.random.default_rng(9)
+    hubs = [11, 70_000, 149_000]
+    src = np.concatenate([src] + [np.full(2500, h, dtype=np.uint32) for h in hubs])
+    dst = np.concatenate([dst] + [rng.choice(n, 2500, replace=False).astype(np.uint32) for _ in hubs])
+    off, tgt, _ = oracle.csr_build(n, src, dst, clean=True)
+    g = cuda.SparseGraph(n, torch.as_tensor(off), torch.as_tensor(tgt.astype(np.int32)))
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.6, degree_exponent=0.85,
+                                edge_frac=0.2, kernel_path="owned")
+    params = cuda.DiffusionParams(target_error=1e-10)
+    state = cuda.init(g, params)
+    cuda.run(g, params, sched, state=state)
+    # edit: 40 new edges out of a hub row and 40 random ones, 20 removals
+    added = [(hubs[0], int(t)) for t in rng.choice(n, 40, replace=False) if int(t) != hubs[0]
+             and not g.has_edge(hubs[0], int(t))]
+    added += [(int(s), int(t)) for s, t in rng.integers(0, n, (40, 2)) if s != t and not g.has_edge(int(s), int(t))]
+    removed = []
+    for e in rng.choice(tgt.size, 20, replace=False):
+        s = int(np.searchsorted(off, e, side="right") - 1)
+        removed.append((s, int(tgt[e])))
+    g2 = cuda.apply_delta(g, cuda.GraphDelta(added=sorted(set(added)), removed=sorted(set(removed))))
+    resumed, _ = update.resume(state, g2, params, sched)
+    fresh, _ = cuda.run(g2, params, sched)
+    assert float(np.abs(resumed - fresh).sum()) <= 4 * params.target_error
