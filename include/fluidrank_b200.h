@@ -27,7 +27,8 @@
 extern "C" {
 #endif
 
-#define FR_ABI_VERSION 2
+/* 3: fr_power_run_profiled fills 4 timings (was 3); fr_ppr_set_pull added */
+#define FR_ABI_VERSION 3
 
 enum fr_status {
     FR_OK = 0,

@@ -97,6 +97,9 @@ SIGNATURES = {
 }
 
 
+ABI_VERSION = 3  # FR_ABI_VERSION of include/fluidrank_b200.h
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -107,6 +110,9 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.fr_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH} has ABI version {lib.fr_abi_version()}, this package binds "
+                          f"{ABI_VERSION} (include/fluidrank_b200.h): rebuild the library")
     return lib
 
 

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_no_device_here():
     import torch
     from paper_1202_6158_b200 import _lib
-    assert _lib.lib.fr_abi_version() == 2
+    assert _lib.lib.fr_abi_version() == 3
     if not torch.cuda.is_available():
         assert _lib.lib.fr_device_sms() == 0
         with pytest.raises(RuntimeError, match="no CPU fallback"):
