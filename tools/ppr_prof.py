@@ -17,18 +17,24 @@ import argparse  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--local-frac", type=float, default=None, help="generator local fraction (diagnostic graphs)")
 ap.add_argument("--mode", default="push", help="push | pull | hybrid")
+ap.add_argument("--decays", default="0.6", help="comma-separated theta decays, one timed solve each")
 args = ap.parse_args()
 if args.local_frac is None:
     g, _ = gen.baseline_graph(4)
 else:
     g, _ = gen.generate(gen.web_config(8.0, local_frac=args.local_frac), 1_000_000, 0, exact=True)
 seeds = fr.config4_seeds(g.n, 64, 10, seed=0)
-p = fr.BatchedPPR(g, 64, 0.85, 1e-9, mode=args.mode)
-p.solve(seeds)
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-rank, st, res = p.solve(seeds)
-e1.record()
-torch.cuda.synchronize()
-print(f"n={g.n} L={g.edge_count} time {e0.elapsed_time(e1):.2f} ms sweeps={st.sweeps} row_visits={st.diffusions} "
-      f"edge_visits={st.elementary_steps} pushes={st.hub_edges} max_residual={max(res):.2e}")
+for dec in [float(x) for x in args.decays.split(",")]:
+    p = fr.BatchedPPR(g, 64, 0.85, 1e-9, decay=dec, mode=args.mode)
+    p.solve(seeds)
+    ts = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rank, st, res = p.solve(seeds)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print(f"n={g.n} L={g.edge_count} decay {dec} time {min(ts):.2f} ms (of {len(ts)}) sweeps={st.sweeps} "
+          f"row_visits={st.diffusions} edge_visits={st.elementary_steps} pushes={st.hub_edges} "
+          f"max_residual={max(res):.2e}")
