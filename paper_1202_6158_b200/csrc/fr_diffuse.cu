@@ -591,8 +591,9 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 // shared-memory copy of the chunk's fluid (acc) instead of red.global.add in
 // L2, and a node reached by such pushes before its own tile is scanned
 // diffuses them in the same sweep (Gauss-Seidel within the chunk; PAPER
-// Theorem 3.1 allows any order).  At the end of the chunk what is left in acc
-// goes back to F with one coalesced red.add per non-zero node.  Pushes that
+// Theorem 3.1 allows any order).  A selected node's take leaves -F_i in acc, so
+// at the end of the chunk one coalesced red.add per non-zero node both removes
+// the taken fluid from F and adds what was pushed there afterwards.  Pushes that
 // leave the chunk, and the slotted hot/warm targets, are handled as in k_sweep.
 #ifndef FR_OWN_NT
 #define FR_OWN_NT 128
@@ -619,6 +620,10 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #define FR_OWN_BULKPF 1  // one bulk L2 prefetch of the chunk's fluid and offsets (0: per-tile prefetches)
 #endif
 
+#ifndef FR_OWN_TAKEACC
+#define FR_OWN_TAKEACC 1  // the take leaves -f in acc (one exchange); the chunk flush subtracts it from F
+#endif
+
 static constexpr int OWN_NT = FR_OWN_NT;
 static constexpr int OWN_UNROLL = FR_OWN_UNROLL;
 static_assert(OWN_UNROLL * 6 <= 32, "packed row indices");
@@ -628,6 +633,12 @@ __device__ __forceinline__ double take_shared(double *p) {
     return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
 }
 __device__ __forceinline__ float take_shared(float *p) { return atomicExch(p, 0.0f); }
+// exchange: returns what was pending and leaves x
+__device__ __forceinline__ double swap_shared(double *p, double x) {
+    return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(p),
+                                                      (unsigned long long)__double_as_longlong(x)));
+}
+__device__ __forceinline__ float swap_shared(float *p, float x) { return atomicExch(p, x); }
 
 // Deferred hub rows (hub_defer): the whole block claims one row queued by the
 // previous sweep and pushes it (128 threads over its columns, as k_push_block;
@@ -776,13 +787,20 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
             sel = sel && valid && f != (FT)0;
             const bool big = deg >= a.t2;
             const bool act = sel && !big && deg > 0;
-            // take: the loaded global fluid by a fire-and-forget subtraction (as
-            // k_sweep), the shared-memory part by exchange (other warps of the
-            // block may be adding to it); what arrives later stays for the flush
+            // take: one shared-memory exchange returns what was pushed here earlier in
+            // this chunk and leaves -fg in its place (other warps of the block keep
+            // adding to it); the chunk flush then subtracts the taken global fluid
+            // from F together with the later pushes in its one red.add per node, so
+            // the take costs no global operation of its own.  F_i keeps fg until the
+            // flush: only this block reads the chunk's F during the sweep.
             FT sent = (FT)0;
             if (sel) {
+#if FR_OWN_TAKEACC
+                const FT ps = swap_shared(acc + li, -fg);
+#else
                 const FT ps = pend != (FT)0 ? take_shared(acc + li) : (FT)0;
                 if (fg != (FT)0) red_add(F + i, -fg);
+#endif
                 sent = fg + ps;
             }
             const u32 adeg = act ? deg : 0u;
