@@ -620,6 +620,10 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #define FR_OWN_BULKPF 1  // one bulk L2 prefetch of the chunk's fluid and offsets (0: per-tile prefetches)
 #endif
 
+#ifndef FR_OWN_RSEARCH
+#define FR_OWN_RSEARCH 1  // row of an edge position from a REDUX/VOTE head mask over lane-compacted rows (0: 5-step shuffle search)
+#endif
+
 #ifndef FR_OWN_TAKEACC
 #define FR_OWN_TAKEACC 1  // the take leaves -f in acc (one exchange); the chunk flush subtracts it from F
 #endif
@@ -828,6 +832,43 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
             // the end) packed 6 bits per batch slot into one register
             u32 tvA[OWN_UNROLL], tvB[OWN_UNROLL], tvC[OWN_UNROLL];
             u32 rvA = 0, rvB = 0, rvC = 0;
+#if FR_OWN_RSEARCH
+            // The active rows are compacted into the low lanes (lane k holds the k-th
+            // active row: its start in the edge space and lo - start, the base its
+            // columns are addressed from), so their starts are strictly increasing and
+            // the row of the 32 positions of a window follows from one REDUX.OR of the
+            // row heads inside the window, one VOTE for the rows at or before it and a
+            // POPC per lane -- no shuffles (they share the L1 data pipe with the
+            // shared-memory atomics, the busiest unit of this kernel).
+            const u32 amask = __ballot_sync(FULL, act);
+            const u32 na = (u32)__popc(amask);
+            int csrc = 0;  // lane of the (lane + 1)-th active row: the largest x with popc(amask below x) <= lane
+#pragma unroll
+            for (int s2 = 16; s2 > 0; s2 >>= 1) {
+                const int x = csrc + s2;
+                if ((u32)__popc(amask & ((1u << x) - 1u)) <= (u32)lane) csrc = x;
+            }
+            const u32 cst0 = __shfl_sync(FULL, start, csrc);
+            const u32 cstart = (u32)lane < na ? cst0 : 0xffffffffu;
+            const OT cbase = __shfl_sync(FULL, (OT)(lo - (OT)start), csrc);
+            auto issue = [&](u32 (&tv)[OWN_UNROLL], u32 &rv, u32 c0) {
+                rv = 0;
+#pragma unroll
+                for (int u = 0; u < OWN_UNROLL; u++) {
+                    const u32 w0 = c0 + (u32)(u * 32);
+                    const u32 t = cstart - w0;  // 1..31: this row's head lies inside the window
+                    const u32 heads = __reduce_or_sync(FULL, (t - 1u < 31u) ? (1u << t) : 0u);
+                    const u32 nb = (u32)__popc(__ballot_sync(FULL, cstart <= w0));  // >= 1: the first row starts at 0
+                    const u32 p0 = w0 + (u32)lane;
+                    const bool in = p0 < total;
+                    const u32 p = in ? p0 : total - 1;
+                    const u32 r = in ? nb + (u32)__popc(heads & ((2u << lane) - 1u)) - 1u : na - 1u;
+                    const OT cb = __shfl_sync(FULL, cbase, (int)r);
+                    rv |= (in ? r + 1u : 0u) << (6 * u);
+                    tv[u] = __ldg(tgt + (cb + (OT)p));
+                }
+            };
+#else
             auto issue = [&](u32 (&tv)[OWN_UNROLL], u32 &rv, u32 c0) {
                 rv = 0;
 #pragma unroll
@@ -846,6 +887,7 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                     tv[u] = __ldg(tgt + rlo + (p - rs));
                 }
             };
+#endif
             constexpr u32 STEP = 32 * OWN_UNROLL;
             // two batches in flight before the first scatter
             if (total) issue(tvA, rvA, 0);
@@ -864,6 +906,11 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                 }
             }
             const FT pvf = (FT)pv;
+#if FR_OWN_RSEARCH
+            const FT spv = __shfl_sync(FULL, pvf, csrc);  // push value of the lane's compacted row
+#else
+            const FT spv = pvf;
+#endif
             const bool hub = sel && big;
             const u32 hmask = __ballot_sync(FULL, hub);
             if (hmask) {
@@ -885,7 +932,7 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
 #pragma unroll
                 for (int u = 0; u < OWN_UNROLL; u++) {
                     const int r = (int)((rv >> (6 * u)) & 63u) - 1;
-                    const FT v = __shfl_sync(FULL, pvf, r < 0 ? 0 : r);
+                    const FT v = __shfl_sync(FULL, spv, r < 0 ? 0 : r);
                     if (r >= 0) {
                         const u32 t = tv[u];
                         const u32 lt2 = t - ubase;
