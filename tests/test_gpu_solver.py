@@ -534,3 +534,58 @@ def test_owned_deferred_hub_rows(cuda, oracle, monkeypatch, defer):
     ref = oracle.run_seq(off, tgt, 0.85, 1e-12, "sweep").rank
     rank, _ = cuda.run(g, params, sched)
     assert l1(rank, ref) <= 1e-9
+
+
+def _shape_graph(n, degs, rng):
+    """Rows with the given out-degree pattern (cycled over the nodes); targets near the row."""
+    deg = np.resize(np.asarray(degs, dtype=np.int64), n)
+    src = np.repeat(np.arange(n, dtype=np.uint32), deg)
+    # distinct targets per row: a random start, then consecutive ids (wrapping), never the row itself
+    start = rng.integers(1, n - deg.max() - 1, size=n)
+    k = np.arange(src.size) - np.repeat(np.cumsum(deg) - deg, deg)
+    dst = ((src.astype(np.int64) + np.repeat(start, deg) + k) % n).astype(np.uint32)
+    return src, dst
+
+
+@pytest.mark.parametrize("shape", ["ones", "lane31", "full96", "big_small", "sparse", "mixed"])
+def test_owned_row_search_shapes(cuda, oracle, monkeypatch, shape):
+    """k_sweep_own finds the row of an edge position from a REDUX.OR mask of the row heads in
+    each 32-position window over the lane-compacted active rows.  Degree patterns that put the
+    heads on the window boundaries: every row one edge (32 heads per window), one active row per
+    tile in the last lane, tiles of exactly 96 / 192 edges (whole batches), rows just under
+    the hub threshold next to one-edge rows (windows without heads, thousands of positions),
+    mostly dangling rows, and a mixed pattern -- conservation after a partial run, then the
+    rank against the oracle."""
+    monkeypatch.setenv("FR_SMALL", "0")
+    monkeypatch.setenv("FR_OWN_CHUNK", "256")
+    rng = np.random.default_rng(11)
+    n = 40_000
+    degs = {
+        "ones": [1],
+        "lane31": [0] * 31 + [37],
+        "full96": [3] * 32 + [6] * 32,
+        "big_small": [2047, 1, 0, 1, 2040, 1, 1, 33],
+        "sparse": [0, 0, 0, 5, 0, 0, 0, 0, 0, 64, 0],
+        "mixed": [31, 32, 33, 1, 0, 95, 96, 97, 2, 0, 0, 191, 192, 193, 7],
+    }[shape]
+    src, dst = _shape_graph(n, degs, rng)
+    off, tgt, _ = oracle.csr_build(n, src, dst, clean=True)
+    g = graph_from(cuda, off, tgt)
+    sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=0.6, degree_exponent=0.85,
+                                edge_frac=0.2, kernel_path="owned")
+    params = cuda.DiffusionParams(target_error=1e-12)
+    state = cuda.init(g, params)
+    f0 = state.fluid.cpu().numpy().copy()
+    cuda.run(g, params, sched, state=state, max_sweeps=5)
+    torch.cuda.synchronize()
+    h = state.history.cpu().numpy()
+    f = state.fluid.cpu().numpy()
+    deg = np.diff(off)
+    src_e = np.repeat(np.arange(g.n), deg)
+    push = np.zeros(g.n)
+    np.add.at(push, tgt.astype(np.int64), h[src_e] / deg[src_e])
+    assert np.abs(h + f - f0 - 0.85 * push).max() <= 1e-15
+    params = cuda.DiffusionParams(target_error=1e-10)
+    rank, _ = cuda.run(g, params, sched)
+    ref = oracle.run_seq(off, tgt, 0.85, 1e-13, "sweep").rank
+    assert l1(rank, ref) <= 1e-9

@@ -38,6 +38,12 @@ for case in range(cases):
     fp32 = rng.random() < 0.25
     beta = rng.choice([0.0, 0.5, 0.65, 1.0]) if kind == "sweep" else 0.0
     damping = rng.choice([0.85, 0.85, 0.5, 0.99])
+    if kind == "max" and damping == 0.99 and n > 40_000:
+        # the max rule diffuses only the nodes within `decay` of the largest fluid (a handful per
+        # sweep on a web graph); at d = 0.99 a 300k-node graph needs > 10^6 such sweeps, the
+        # solver's cap (seed 13, case 5: NoConvergenceError on every path and precision alike,
+        # tools/repro_max.py) -- a property of the rule, not a parity case
+        damping = 0.85
     target = 1e-8 if fp32 else 1e-10
     os.environ["FR_SMALL"] = small
     g = fr.SparseGraph(n, torch.as_tensor(off), torch.as_tensor(tgt.astype(np.int32)))
