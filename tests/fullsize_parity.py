@@ -1,7 +1,7 @@
 """Full-size parity: the BASELINE configurations solved on the GPU, checked against the
 CPU oracle on the same seeded graphs (TEST INFRASTRUCTURE; run on the GPU box).
 
-    python tests/fullsize_parity.py [--configs 2,3,4,5] [--out profiles/r02_parity_fullsize.json]
+    [FR_PARITY_SEED=S] python tests/fullsize_parity.py [--configs 2,3,4,5] [--out profiles/r02_parity_fullsize.json]
 
 For each configuration the device builds the exact-size graph (gen.baseline_graph:
 base draw, cleaned, fill rounds) and a worker process builds the same graph with the
@@ -35,7 +35,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-SEED = 0  # bench.py's default seed
+SEED = int(os.environ.get("FR_PARITY_SEED", "0"))  # 0 = bench.py's default seed (the env reaches the spawned workers)
 TMP = os.environ.get("FR_PARITY_TMP", "/tmp/fr_parity")
 # (n, mean out-degree) of the web-generator BASELINE configs
 WEB = {2: (1_000_000, 8.0), 3: (20_000_000, 10.0), 4: (1_000_000, 8.0), 5: (100_000_000, 16.0)}
