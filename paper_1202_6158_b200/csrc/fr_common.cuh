@@ -164,6 +164,16 @@ __device__ __forceinline__ void red_add(float *p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// Fire-and-forget shared-memory add at a 32-bit shared-window address (ptxas expands it to
+// the LDS + ATOMS.CAST.SPIN loop of atomicAdd, addressed from the caller's register instead
+// of a shared base it re-derives at every site).
+__device__ __forceinline__ void shared_red_add(u32 saddr, double v) {
+    asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(saddr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void shared_red_add(u32 saddr, float v) {
+    asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(saddr), "f"(v) : "memory");
+}
+
 // Fire-and-forget global add with an L2 cache-policy hint (createpolicy).
 __device__ __forceinline__ void red_add_hint(double *p, double v, u64 pol) {
     asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");

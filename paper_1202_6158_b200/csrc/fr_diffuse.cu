@@ -624,6 +624,10 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #define FR_OWN_RSEARCH 1  // row of an edge position from a REDUX/VOTE head mask over lane-compacted rows (0: 5-step shuffle search)
 #endif
 
+#ifndef FR_OWN_UNISCAT
+#define FR_OWN_UNISCAT 2  // scatter with one shared-memory add (chunk + hot tables) and one global red.add (warm + near)
+#endif
+
 #ifndef FR_OWN_TAKEACC
 #define FR_OWN_TAKEACC 1  // the take leaves -f in acc (one exchange); the chunk flush subtracts it from F
 #endif
@@ -707,6 +711,16 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
     FT *__restrict__ F = a.F;
 #if FR_COLD_HINT
     const u64 cold_pol = policy_evict_first();
+#endif
+#if FR_OWN_UNISCAT
+    u32 sbase = (u32)__cvta_generic_to_shared(acc);
+    asm volatile("mov.u32 %0, %0;" : "+r"(sbase));  // kept in a register (else re-derived at every add)
+    u32 fmask = a.nslots != 0 ? HOT_FLAG : 0u;
+    u32 hot_end = a.own_ch + a.nhot;
+#if FR_OWN_UNISCAT > 1
+    asm volatile("mov.u32 %0, %0;" : "+r"(fmask));
+    asm volatile("mov.u32 %0, %0;" : "+r"(hot_end));
+#endif
 #endif
     for (u32 q = threadIdx.x; q < CH; q += OWN_NT) acc[q] = (FT)0;
     hot_clear(hot_acc, a.nhot, OWN_NT);
@@ -936,6 +950,20 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                     if (r >= 0) {
                         const u32 t = tv[u];
                         const u32 lt2 = t - ubase;
+#if FR_OWN_UNISCAT
+                        // two destinations in shared memory (the chunk table, the hot table right
+                        // behind it) share one add; the warm and the near unslotted global targets
+                        // share one red.add; the cold ones keep their own (uniform policy operand)
+                        const u32 tf = t & fmask;  // != 0: a slotted target
+                        const u32 sl = t ^ tf;     // its slot, or the node id itself
+                        const u32 idx = tf ? CH + sl : lt2;
+                        if (idx < (tf ? hot_end : len)) shared_red_add(sbase + idx * (u32)sizeof(FT), v);
+#if FR_COLD_HINT
+                        else if (!tf && (lt2 + 4096u) > CH + 8192u) red_add_hint(F + t, v, cold_pol);
+#endif
+                        else red_add((tf ? a.Fw : F) + sl, v);
+                        continue;
+#endif
                         if (!(slotted && (t & HOT_FLAG)) && lt2 < len) atomicAdd(acc + lt2, v);  // inside the chunk
 #if FR_COLD_HINT
                         else if (!(slotted && (t & HOT_FLAG)) && (t - ubase + 4096u) > CH + 8192u)

@@ -107,3 +107,43 @@ def test_node_ids_above_2_31(cuda, oracle):
     low = h[:base]
     assert float((low - 0.15 / n).abs().max()) <= 1e-24
     assert state.residual <= 1e-10 * 0.15
+
+
+@pytest.mark.timeout(900)
+def test_bench_kernel_configuration_vs_oracle(cuda, oracle):
+    """The config-5 generator (mean out-degree 16) scaled to 4.5M nodes: large enough for
+    everything the benchmarked solve uses -- the owned path's default 2048-node chunks (n >=
+    ~2.7M), the sampled in-degree of the slot classes and the 8-piece host copy (m >= 2^26),
+    deferred hub rows -- and small enough for the CPU oracle in the default GPU suite.
+    Bit-exact CSR; rank L1 <= 1e-9 against the oracle's sequential reference run with the
+    exact bench schedules (d = 0.85: adaptive 0.6 / 0.2; d = 0.99: 0.7 / 0.15; beta 0.85),
+    resident and through fr_pagerank_host.  The 100M-node record is
+    profiles/r02_parity_fullsize_final2.json (tests/fullsize_parity.py)."""
+    import ctypes
+
+    from paper_1202_6158_b200 import _lib, gen
+    n, seed = 4_500_000, 5
+    g, rep = gen.baseline_graph(5, seed=seed, n=n)
+    off, tgt, orep = oracle.gen_graph_exact(oracle.web_config(16.0), n, seed)
+    assert g.edge_count >= 1 << 26
+    assert np.array_equal(g.out_offsets.cpu().numpy(), off)
+    assert np.array_equal(g.out_targets.cpu().numpy().view(np.uint32), tgt)
+    assert (rep.realized_links, rep.duplicates, rep.self_loops, rep.rounds, rep.unfilled) == (
+        orep["realized_links"], orep["duplicates"], orep["self_loops"], orep["rounds"], orep["unfilled"])
+    for d, decay, ef in ((0.85, 0.6, 0.2), (0.99, 0.7, 0.15)):
+        ref = oracle.run_seq(off, tgt, d, 1e-12, "sweep").rank
+        sched = cuda.make_scheduler("sweep", policy="adaptive", sweep_decay=decay, edge_frac=ef,
+                                    degree_exponent=0.85, kernel_path="owned")
+        params = cuda.DiffusionParams(damping=d, target_error=1e-9)
+        rank, trace = cuda.run(g, params, sched)
+        assert trace.rows[-1].residual <= 1e-9 * (1.0 - d)
+        assert float(np.abs(rank - ref).sum()) <= 1e-9
+        if d == 0.85:
+            cfg = sched.solver_config(params)
+            hr = np.empty(n)
+            st = _lib.SolveStats()
+            h_off = np.ascontiguousarray(off)
+            h_tgt = np.ascontiguousarray(tgt)
+            _lib.check(_lib.lib.fr_pagerank_host(n, h_tgt.size, h_off.ctypes.data, h_tgt.ctypes.data, None,
+                                                 ctypes.byref(cfg), hr.ctypes.data, ctypes.byref(st)))
+            assert float(np.abs(hr - ref).sum()) <= 1e-9
