@@ -174,6 +174,29 @@ __device__ __forceinline__ void shared_red_add(u32 saddr, float v) {
     asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(saddr), "f"(v) : "memory");
 }
 
+// Two predicated fire-and-forget global adds in one block (no branches): plain when `plain`,
+// with the L2 cache-policy hint when `hinted`; neither flag set: nothing is issued.
+__device__ __forceinline__ void red_add_pred2(double *p, double v, u64 pol, bool plain, bool hinted) {
+    asm volatile(
+        "{\n\t.reg .pred pn, pc;\n\t"
+        "setp.ne.u32 pn, %3, 0;\n\t"
+        "setp.ne.u32 pc, %4, 0;\n\t"
+        "@pn red.global.add.f64 [%0], %1;\n\t"
+        "@pc red.global.add.L2::cache_hint.f64 [%0], %1, %2;\n\t}"
+        ::"l"(p), "d"(v), "l"(pol), "r"((u32)plain), "r"((u32)hinted)
+        : "memory");
+}
+__device__ __forceinline__ void red_add_pred2(float *p, float v, u64 pol, bool plain, bool hinted) {
+    asm volatile(
+        "{\n\t.reg .pred pn, pc;\n\t"
+        "setp.ne.u32 pn, %3, 0;\n\t"
+        "setp.ne.u32 pc, %4, 0;\n\t"
+        "@pn red.global.add.f32 [%0], %1;\n\t"
+        "@pc red.global.add.L2::cache_hint.f32 [%0], %1, %2;\n\t}"
+        ::"l"(p), "f"(v), "l"(pol), "r"((u32)plain), "r"((u32)hinted)
+        : "memory");
+}
+
 // Fire-and-forget global add with an L2 cache-policy hint (createpolicy).
 __device__ __forceinline__ void red_add_hint(double *p, double v, u64 pol) {
     asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");

@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(SW_NT, FR_SW_MINB) k_sweep(SweepArgs<FT> a) {
 #endif
 
 #ifndef FR_OWN_UNISCAT
-#define FR_OWN_UNISCAT 2  // scatter with one shared-memory add (chunk + hot tables) and one global red.add (warm + near)
+#define FR_OWN_UNISCAT 3  // scatter: one shared-memory add (chunk + hot tables), one global red.add (warm + near); 3: the global adds predicated
 #endif
 
 #ifndef FR_OWN_TAKEACC
@@ -711,6 +711,10 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
     FT *__restrict__ F = a.F;
 #if FR_COLD_HINT
     const u64 cold_pol = policy_evict_first();
+#endif
+    u32 lemask = (2u << lane) - 1u;  // lanes at or below this one
+#if FR_OWN_UNISCAT > 3
+    asm volatile("mov.u32 %0, %0;" : "+r"(lemask));  // kept in a register
 #endif
 #if FR_OWN_UNISCAT
     u32 sbase = (u32)__cvta_generic_to_shared(acc);
@@ -876,7 +880,7 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                     const u32 p0 = w0 + (u32)lane;
                     const bool in = p0 < total;
                     const u32 p = in ? p0 : total - 1;
-                    const u32 r = in ? nb + (u32)__popc(heads & ((2u << lane) - 1u)) - 1u : na - 1u;
+                    const u32 r = in ? nb + (u32)__popc(heads & lemask) - 1u : na - 1u;
                     const OT cb = __shfl_sync(FULL, cbase, (int)r);
                     rv |= (in ? r + 1u : 0u) << (6 * u);
                     tv[u] = __ldg(tgt + (cb + (OT)p));
@@ -957,6 +961,14 @@ __global__ void __launch_bounds__(OWN_NT, WIDE ? 8 : FR_OWN_MINB) k_sweep_own(Sw
                         const u32 tf = t & fmask;  // != 0: a slotted target
                         const u32 sl = t ^ tf;     // its slot, or the node id itself
                         const u32 idx = tf ? CH + sl : lt2;
+#if FR_OWN_UNISCAT > 2 && FR_COLD_HINT
+                        // the global adds predicated (no branch around them), then the shared-memory lanes
+                        const bool sh = idx < (tf ? hot_end : len);
+                        const bool cold = !tf && (lt2 + 4096u) > CH + 8192u;
+                        red_add_pred2((tf ? a.Fw : F) + sl, v, cold_pol, !sh && !cold, !sh && cold);
+                        if (sh) shared_red_add(sbase + idx * (u32)sizeof(FT), v);
+                        continue;
+#endif
                         if (idx < (tf ? hot_end : len)) shared_red_add(sbase + idx * (u32)sizeof(FT), v);
 #if FR_COLD_HINT
                         else if (!tf && (lt2 + 4096u) > CH + 8192u) red_add_hint(F + t, v, cold_pol);
